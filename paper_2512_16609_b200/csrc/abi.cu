@@ -1,0 +1,171 @@
+// C ABI of libdehaze_b200.so (see include/dehaze_b200.h).
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <cstdarg>
+#include <string>
+
+#include "../../include/dehaze_b200.h"
+#include "dhz_common.cuh"
+#include "dhz_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(DHZ_E_CUDA, "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+constexpr int64_t kAlign = 256;
+int64_t align_up(int64_t v, int64_t a = kAlign) { return (v + a - 1) / a * a; }
+
+struct Layout {
+  int64_t frame_max, sel, seg_hist, seg_meta, seg_full, sel_idx, lut, dark, tmap, total;
+  int64_t dark_fs;
+  int S;
+};
+
+Layout make_layout(int n, int H, int W, const dhz_params* p) {
+  Layout L{};
+  const int64_t npx = (int64_t)H * W;
+  L.S = (int)((npx + dhz::kSeg - 1) / dhz::kSeg);
+  L.dark_fs = align_up(npx, 16);
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t at = o;
+    o = align_up(o + bytes);
+    return at;
+  };
+  L.frame_max = take(4LL * n);
+  L.sel = take((int64_t)sizeof(dhz::FrameSel) * n);
+  L.seg_hist = take(4LL * n * L.S * dhz::kWin);
+  L.seg_meta = take(16LL * n * L.S);
+  L.seg_full = take(1024LL * n * L.S);
+  L.sel_idx = take(4LL * n * std::max<int64_t>(1, p->top_k));
+  L.lut = take(3LL * dhz::kTri * n);
+  L.dark = take(L.dark_fs * n);
+  L.tmap = -1;
+  if (p->mode == 1) L.tmap = take(8LL * npx * n);
+  L.total = o;
+  return L;
+}
+
+int check_params(int n, int H, int W, const dhz_params* p) {
+  if (!p) return fail(DHZ_E_INVALID, "params is NULL");
+  if (n < 0) return fail(DHZ_E_INVALID, "n_frames must be >= 0, got %d", n);
+  if (H < 1 || W < 1) return fail(DHZ_E_INVALID, "empty frame %dx%d", W, H);
+  const int64_t npx = (int64_t)H * W;
+  if (npx > 0xFFFFFFF0LL) return fail(DHZ_E_INVALID, "frame too large (%lld px)", (long long)npx);
+  if (p->top_k < 1 || p->top_k > npx)
+    return fail(DHZ_E_INVALID, "top_k must lie in [1, %lld], got %lld", (long long)npx, (long long)p->top_k);
+  if (p->patch_radius < 1) return fail(DHZ_E_INVALID, "patch_radius must be >= 1");
+  if (!p->thresholds) return fail(DHZ_E_INVALID, "thresholds table is NULL");
+  if (p->mode != 0 && p->mode != 1) return fail(DHZ_E_INVALID, "mode must be 0 or 1");
+  return DHZ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dhz_last_error(void) { return g_err.c_str(); }
+
+int dhz_abi_version(void) { return DHZ_ABI_VERSION; }
+
+int dhz_device_count(void) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n < 1) {
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    return fail(DHZ_E_CUDA, "no CUDA device visible");
+  }
+  return n;
+}
+
+size_t dhz_frames_u8_workspace(int n, int height, int width, const dhz_params* p) {
+  if (check_params(std::max(n, 0), height, width, p) != DHZ_OK) return 0;
+  return (size_t)make_layout(n, height, width, p).total;
+}
+
+int dhz_frames_u8_layout(int n, int height, int width, const dhz_params* p, int64_t* off) {
+  int rc = check_params(n, height, width, p);
+  if (rc) return rc;
+  if (!off) return fail(DHZ_E_INVALID, "offsets is NULL");
+  const Layout L = make_layout(n, height, width, p);
+  off[0] = L.dark;
+  off[1] = L.dark_fs;
+  off[2] = L.sel_idx;
+  off[3] = L.tmap;
+  off[4] = L.total;
+  return DHZ_OK;
+}
+
+int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const dhz_params* p, uint8_t* out,
+                  int64_t out_fs, double* airlight, void* ws, size_t ws_bytes, void* stream,
+                  void* const* events) {
+  int rc = check_params(n, H, W, p);
+  if (rc) return rc;
+  if (n == 0) return DHZ_OK;
+  if (!in || !out || !airlight) return fail(DHZ_E_INVALID, "NULL array argument");
+  const int64_t npx = (int64_t)H * W;
+  if (in_fs < 3 * npx || out_fs < 3 * npx) return fail(DHZ_E_INVALID, "frame stride smaller than a frame");
+  const Layout L = make_layout(n, H, W, p);
+  if (!ws || (int64_t)ws_bytes < L.total)
+    return fail(DHZ_E_WORKSPACE, "workspace too small: need %lld bytes, got %zu", (long long)L.total, ws_bytes);
+  if (p->mode != 0) return fail(DHZ_E_UNSUPPORTED, "image mode is not available in this build");
+  if (p->balance) return fail(DHZ_E_UNSUPPORTED, "gray-world balance is not available in this build");
+  if (dhz::dark_u8_max_smem(p->patch_radius) > 200 * 1024)
+    return fail(DHZ_E_UNSUPPORTED, "patch_radius %d too large for the tiled erosion", p->patch_radius);
+
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  auto mark = [&](int i) {
+    if (events && events[i]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[i]), st);
+  };
+  mark(0);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  cudaError_t e = cudaMemsetAsync(base, 0, (size_t)L.seg_hist, st);  // frame_max + sel records
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+
+  uint8_t* dark = base + L.dark;
+  uint32_t* fmax = reinterpret_cast<uint32_t*>(base + L.frame_max);
+  e = dhz::dark_u8(in, in_fs, n, H, W, p->patch_radius, dark, L.dark_fs, fmax, st);
+  if (e != cudaSuccess) return cuda_fail(e, "dark_u8");
+  mark(1);
+
+  dhz::SelectWs sw{};
+  sw.sel = reinterpret_cast<dhz::FrameSel*>(base + L.sel);
+  sw.frame_max = fmax;
+  sw.seg_hist = reinterpret_cast<uint32_t*>(base + L.seg_hist);
+  sw.seg_full = reinterpret_cast<uint32_t*>(base + L.seg_full);
+  sw.seg_meta = reinterpret_cast<uint32_t*>(base + L.seg_meta);
+  sw.sel_idx = reinterpret_cast<uint32_t*>(base + L.sel_idx);
+  sw.S = L.S;
+  e = dhz::select_u8(dark, L.dark_fs, n, npx, p->top_k, sw, st);
+  if (e != cudaSuccess) return cuda_fail(e, "select_u8");
+  e = dhz::airlight_sum_u8(in, in_fs, n, npx, p->top_k, p->alpha, sw, airlight, st);
+  if (e != cudaSuccess) return cuda_fail(e, "airlight_sum_u8");
+  mark(2);
+
+  uint8_t* lut = base + L.lut;
+  e = dhz::build_lut_u8(n, airlight, p->omega, p->t_min, p->thresholds, lut, st);
+  if (e != cudaSuccess) return cuda_fail(e, "build_lut_u8");
+  mark(3);
+  e = dhz::recover_lut_u8(in, in_fs, n, H, W, lut, out, out_fs, st);
+  if (e != cudaSuccess) return cuda_fail(e, "recover_lut_u8");
+  mark(4);
+  return DHZ_OK;
+}
+
+}  // extern "C"

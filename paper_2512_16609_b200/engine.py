@@ -1,0 +1,129 @@
+"""Device-side batch engine: owns workspaces and launches the fused frame pipeline.
+
+Frames live in HBM as one contiguous uint8 tensor (n, H, W, 3); one call of
+``FrameEngine.run`` enqueues the whole batch (K1 dark -> K2..K4 top-K select +
+airlight -> K5 LUT -> K6 recover) on a CUDA stream through the
+C ABI.  Nothing here touches pixel data on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import threading
+
+import torch
+
+from . import _native
+from .quant import device_thresholds
+
+
+def top_k(npx: int, top_fraction: float) -> int:
+    """estimation.py:72 — K = max(1, floor(top_fraction * n)), Python float arithmetic."""
+    return max(1, math.floor(top_fraction * npx))
+
+
+def native_params(params, npx: int, thresholds: torch.Tensor) -> _native.DhzParams:
+    p = _native.DhzParams()
+    p.mode = 1 if params.mode == "image" else 0
+    p.patch_radius = int(params.patch_radius)
+    p.top_k = top_k(npx, params.top_fraction)
+    p.alpha = float(params.alpha)
+    p.omega = float(params.omega)
+    p.t_min = float(params.t_min)
+    p.guided_radius = int(params.guided_radius)
+    p.balance = 1 if params.balance_enabled() else 0
+    p.guided_eps = float(params.guided_eps)
+    p.gamma = float(params.gamma)
+    p.thresholds = thresholds.data_ptr()
+    return p
+
+
+class FrameEngine:
+    """Runs the fused u8 pipeline over device-resident frame batches on one GPU."""
+
+    def __init__(self, device=None):
+        self.lib = _native.lib()
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
+        self._ws = None
+        self._lock = threading.Lock()
+
+    def workspace(self, nbytes: int) -> torch.Tensor:
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def layout(self, n, H, W, p):
+        off = (ctypes.c_int64 * 5)()
+        _native.check(self.lib.dhz_frames_u8_layout(n, H, W, ctypes.byref(p), off), "dhz_frames_u8_layout")
+        return list(off)
+
+    def run(self, frames: torch.Tensor, params, out: torch.Tensor | None = None,
+            airlight: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None,
+            keep_maps: bool = False, events=None):
+        """Dehaze ``frames`` (n, H, W, 3) uint8 CUDA, C-contiguous.
+
+        Returns (out uint8 (n, H, W, 3), airlight float64 (n, 3)) as CUDA tensors,
+        plus a dict of device maps when ``keep_maps`` (dark u8, selected indices).
+        """
+        if frames.dim() != 4 or frames.shape[-1] != 3 or frames.dtype != torch.uint8:
+            raise ValueError(f"frames must be (n, H, W, 3) uint8, got {tuple(frames.shape)} {frames.dtype}")
+        if not frames.is_cuda:
+            raise ValueError("frames must be a CUDA tensor")
+        frames = frames.contiguous()
+        n, H, W, _ = frames.shape
+        dev = frames.device
+        thr = device_thresholds(params.gamma, dev)
+        p = native_params(params, H * W, thr)
+        if out is None:
+            out = torch.empty_like(frames)
+        if airlight is None:
+            airlight = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        ev_arr = None
+        if events is not None:
+            # torch creates events lazily: record once so each has a handle, then
+            # let the library re-record them between the fused stages.
+            for ev in events:
+                ev.record(st)
+            ev_arr = (ctypes.c_void_p * len(events))(*[ev.cuda_event for ev in events])
+        with self._lock:
+            nbytes = self.lib.dhz_frames_u8_workspace(n, H, W, ctypes.byref(p))
+            if nbytes == 0:
+                _native.check(_native.DHZ_E_INVALID, "dhz_frames_u8_workspace")
+            ws = self.workspace(nbytes)
+            rc = self.lib.dhz_frames_u8(
+                frames.data_ptr(), 3 * H * W, n, H, W, ctypes.byref(p), out.data_ptr(), 3 * H * W,
+                airlight.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream, ev_arr)
+            _native.check(rc, "dhz_frames_u8")
+            maps = None
+            if keep_maps:
+                off = self.layout(n, H, W, p)
+                dark_fs = off[1]
+                dark = ws[off[0]: off[0] + dark_fs * n].view(n, dark_fs)[:, : H * W].reshape(n, H, W).clone()
+                k = p.top_k
+                sel = ws[off[2]: off[2] + 4 * n * k].view(torch.int32).view(n, k).clone()
+                maps = {"dark_u8": dark, "selected": sel}
+        if keep_maps:
+            return out, airlight, maps
+        return out, airlight
+
+
+_engines: dict = {}
+_engines_lock = threading.Lock()
+
+
+def engine_for(device=None) -> FrameEngine:
+    """Per-(device, thread) engine so concurrent callers never share a workspace."""
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    key = (device.index, threading.get_ident())
+    with _engines_lock:
+        eng = _engines.get(key)
+        if eng is None:
+            eng = FrameEngine(device)
+            _engines[key] = eng
+    return eng

@@ -1,0 +1,427 @@
+"""Per-frame dehazing pipeline and stream orchestration (drop-in for reference pipeline.py).
+
+Same public surface as ``/root/reference/pkg/src/dehaze/pipeline.py``:
+``DehazeParams`` (:52-114), ``FrameTelemetry`` (:117-150), ``StreamStats``
+(:153-160), ``dehaze_frame`` (:163-216), ``dehaze_image`` (:219-229),
+``process_stream`` (:232-308), ``VIDEO_STAGES`` / ``IMAGE_STAGES`` (:39-49).
+
+The compute runs on the GPU through libdehaze_b200.so:
+
+* u8 frames at native size (``resize_to`` None or equal to the frame size):
+  the fused batch pipeline (engine.FrameEngine, one C-ABI call per batch);
+* frames that need the bilinear resize (the reference default
+  ``resize_to=(640, 480)``) go through the float64 device path
+  (``floatpath``), which keeps the reference's float64 semantics.
+
+``process_stream`` batches frames on the device instead of fanning them out to
+CPU threads; ``workers`` keeps its contract (validated, results bit-identical
+for every value) but no longer changes the schedule.  Additions (all default
+to reference behaviour): ``dehaze_batch`` for device-resident batches, and the
+``device=`` keyword.
+"""
+
+from __future__ import annotations
+
+import time
+from contextlib import contextmanager
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from .estimation import (
+    DEFAULT_ALPHA,
+    DEFAULT_GUIDED_EPS,
+    DEFAULT_GUIDED_RADIUS,
+    DEFAULT_OMEGA,
+    DEFAULT_PATCH_RADIUS,
+    DEFAULT_T_MIN,
+    DEFAULT_TOP_FRACTION,
+)
+from .recover import DEFAULT_GAMMA
+from .validation import check_u8_frame
+
+DEFAULT_STREAM_SIZE = (640, 480)
+
+VIDEO_STAGES = (
+    "resize",
+    "channel_min",
+    "min_filter",
+    "airlight",
+    "transmission",
+    "recover",
+    "postprocess",
+    "output",
+)
+IMAGE_STAGES = VIDEO_STAGES[:5] + ("guided_filter",) + VIDEO_STAGES[5:]
+
+# How fused device work is attributed to the reference's stage names: the time
+# between consecutive ABI events goes to the first stage of each group; the
+# other stages of the group are recorded with 0.0 s (they run inside the same
+# kernel).  Event order: see include/dehaze_b200.h (DHZ_N_EVENTS).
+_STAGE_GROUPS_VIDEO = (("min_filter", "resize", "channel_min"), ("airlight",), ("transmission",),
+                       ("recover", "postprocess", "output"))
+_STAGE_GROUPS_IMAGE = (("min_filter", "resize", "channel_min"), ("airlight",),
+                       ("guided_filter", "transmission"), ("recover", "postprocess", "output"))
+
+
+@dataclass(frozen=True)
+class DehazeParams:
+    """Hyperparameters for the dehazing pipeline (reference pipeline.py:52-114).
+
+    mode selects the stage set: "video" (no transmission refinement, frames
+    resized to resize_to) or "image" (guided-filter refinement, native
+    resolution unless resize_to is set). white_balance=None means the mode
+    default: off for video, on for image.
+    """
+
+    mode: str = "video"
+    patch_radius: int = DEFAULT_PATCH_RADIUS
+    top_fraction: float = DEFAULT_TOP_FRACTION
+    alpha: float = DEFAULT_ALPHA
+    omega: float = DEFAULT_OMEGA
+    t_min: float = DEFAULT_T_MIN
+    guided_radius: int = DEFAULT_GUIDED_RADIUS
+    guided_eps: float = DEFAULT_GUIDED_EPS
+    gamma: float = DEFAULT_GAMMA
+    white_balance: bool = None
+    resize_to: tuple = DEFAULT_STREAM_SIZE
+
+    @classmethod
+    def for_image(cls, **overrides):
+        """Parameters for single-image work: refine t, keep native size."""
+        overrides.setdefault("mode", "image")
+        overrides.setdefault("resize_to", None)
+        return cls(**overrides)
+
+    def validate(self):
+        if self.mode not in ("video", "image"):
+            raise ValueError(f"mode must be 'video' or 'image', got {self.mode!r}")
+        if int(self.patch_radius) != self.patch_radius or self.patch_radius < 1:
+            raise ValueError(f"patch_radius must be an integer >= 1, got {self.patch_radius}")
+        if not 0.0 < self.top_fraction <= 1.0:
+            raise ValueError(f"top_fraction must lie in (0, 1], got {self.top_fraction}")
+        if not 0.0 < self.alpha <= 1.0:
+            raise ValueError(f"alpha must lie in (0, 1], got {self.alpha}")
+        if not 0.0 < self.omega <= 1.0:
+            raise ValueError(f"omega must lie in (0, 1], got {self.omega}")
+        if not 0.0 < self.t_min < 1.0:
+            raise ValueError(f"t_min must lie in (0, 1), got {self.t_min}")
+        if int(self.guided_radius) != self.guided_radius or self.guided_radius < 1:
+            raise ValueError(f"guided_radius must be an integer >= 1, got {self.guided_radius}")
+        if not self.guided_eps > 0.0:
+            raise ValueError(f"guided_eps must be positive, got {self.guided_eps}")
+        if not self.gamma > 0.0:
+            raise ValueError(f"gamma must be positive, got {self.gamma}")
+        if self.white_balance not in (None, True, False):
+            raise ValueError(f"white_balance must be None or bool, got {self.white_balance!r}")
+        if self.resize_to is not None:
+            try:
+                w, h = self.resize_to
+            except (TypeError, ValueError):
+                raise ValueError(f"resize_to must be None or (width, height), got {self.resize_to!r}")
+            if int(w) != w or int(h) != h or w < 1 or h < 1:
+                raise ValueError(f"resize_to must hold positive integers, got {self.resize_to!r}")
+        return self
+
+    def balance_enabled(self):
+        if self.white_balance is None:
+            return self.mode == "image"
+        return self.white_balance
+
+
+class FrameTelemetry:
+    """Per-stage time and call counts, plus the airlight trace (reference pipeline.py:117-150).
+
+    Stage times of the fused device path are CUDA-event times (seconds); see
+    ``_STAGE_GROUPS_*`` for how fused kernels map onto the stage names.
+    """
+
+    def __init__(self, capture_maps=False):
+        self.timings = {}
+        self.counts = {}
+        self.airlights = []
+        self.capture_maps = capture_maps
+        self.maps = {}
+
+    @contextmanager
+    def stage(self, name):
+        start = time.perf_counter()
+        try:
+            yield
+        finally:
+            self.add_time(name, time.perf_counter() - start)
+
+    def add_time(self, name, seconds):
+        self.timings.setdefault(name, []).append(float(seconds))
+        self.counts[name] = self.counts.get(name, 0) + 1
+
+    def record_airlight(self, airlight):
+        self.airlights.append(np.asarray(airlight, dtype=np.float64).copy())
+
+    def record_map(self, name, m):
+        if self.capture_maps:
+            self.maps[name] = np.array(m, dtype=np.float64, copy=True)
+
+    def total_time(self, name):
+        return sum(self.timings.get(name, ()))
+
+
+@dataclass
+class StreamStats:
+    """Summary of one stream run."""
+
+    frame_count: int
+    wall_time: float
+    fps: float
+    airlight_trace: list = field(default_factory=list)
+
+
+def _needs_resize(params, h, w):
+    if params.resize_to is None:
+        return False
+    rw, rh = params.resize_to
+    return (int(rw), int(rh)) != (w, h)
+
+
+def _as_device_batch(frames_np, device):
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(frames_np))
+    return t.to(device=device, non_blocking=False)
+
+
+def _run_native(batch, params, telemetry=None, keep_maps=False):
+    """batch: (n, H, W, 3) uint8 CUDA tensor at its working size."""
+    import torch
+
+    from .engine import engine_for
+
+    eng = engine_for(batch.device)
+    if telemetry is None:
+        return eng.run(batch, params, keep_maps=keep_maps)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    res = eng.run(batch, params, keep_maps=keep_maps, events=evs)
+    evs[-1].synchronize()
+    groups = _STAGE_GROUPS_IMAGE if params.mode == "image" else _STAGE_GROUPS_VIDEO
+    for i, grp in enumerate(groups):
+        dt = evs[i].elapsed_time(evs[i + 1]) / 1000.0
+        telemetry.add_time(grp[0], max(dt, 0.0))
+        for other in grp[1:]:
+            telemetry.add_time(other, 0.0)
+    return res
+
+
+def _device():
+    import torch
+
+    from . import _native
+
+    _native.lib()  # fail loudly without the library / a CUDA device
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def dehaze_frame(frame, params=None, telemetry=None):
+    """Dehaze one interleaved uint8 RGB frame; returns a uint8 frame (reference pipeline.py:163-216).
+
+    Accepts a numpy array (returns numpy) or a CUDA uint8 tensor (returns a
+    CUDA tensor, no host copies).  Pure: equal inputs give bit-equal outputs.
+    """
+    if params is None:
+        params = DehazeParams()
+    params.validate()
+    tel = telemetry if telemetry is not None else FrameTelemetry()
+    frame = check_u8_frame(frame)
+    is_tensor = not isinstance(frame, np.ndarray)
+    dev = frame.device if is_tensor else _device()
+    h, w = int(frame.shape[0]), int(frame.shape[1])
+    if _needs_resize(params, h, w):
+        from .floatpath import dehaze_float_frame
+
+        out, airlight, maps = dehaze_float_frame(frame if is_tensor else _as_device_batch(frame, dev)[0],
+                                                 params, tel)
+    else:
+        batch = frame[None] if is_tensor else _as_device_batch(frame[None], dev)
+        want_maps = tel.capture_maps
+        res = _run_native(batch, params, tel, keep_maps=want_maps)
+        out, airlight = res[0][0], res[1][0]
+        maps = None
+        if want_maps:
+            from .floatpath import maps_from_native
+
+            maps = maps_from_native(batch[0], res[2], airlight, params)
+    a_host = airlight.detach().cpu().numpy()
+    tel.record_airlight(a_host)
+    if maps is not None:
+        for name in ("dark", "transmission_coarse", "transmission"):
+            tel.record_map(name, maps[name])
+    if is_tensor:
+        return out
+    return out.cpu().numpy()
+
+
+def dehaze_image(frame, params=None, telemetry=None):
+    """Dehaze a single image at native resolution with refinement on (reference pipeline.py:219-229)."""
+    if params is None:
+        params = DehazeParams.for_image()
+    elif params.mode != "image":
+        params = replace(params, mode="image")
+    return dehaze_frame(frame, params, telemetry)
+
+
+def dehaze_batch(frames, params=None, out=None):
+    """Dehaze a device-resident batch (n, H, W, 3) uint8 CUDA tensor in one pipeline launch.
+
+    Returns (out, airlight) CUDA tensors: out (n, H', W', 3) uint8, airlight
+    (n, 3) float64.  Frames that need a resize go through the float path.
+    """
+    if params is None:
+        params = DehazeParams()
+    params.validate()
+    n, h, w = int(frames.shape[0]), int(frames.shape[1]), int(frames.shape[2])
+    if _needs_resize(params, h, w):
+        import torch
+
+        from .floatpath import dehaze_float_frame
+
+        outs, airs = [], []
+        for i in range(n):
+            o, a, _ = dehaze_float_frame(frames[i], params, None)
+            outs.append(o)
+            airs.append(a)
+        return torch.stack(outs), torch.stack(airs)
+    from .engine import engine_for
+
+    return engine_for(frames.device).run(frames, params, out=out)
+
+
+class _HostPipe:
+    """Per-(device, shape) ring of stream slots for host-resident batches."""
+
+    def __init__(self, dev, chunk, H, W, slots=3):
+        import torch
+
+        from .engine import FrameEngine
+
+        self.streams = [torch.cuda.Stream(dev) for _ in range(slots)]
+        self.engines = [FrameEngine(dev) for _ in range(slots)]
+        self.din = [torch.empty((chunk, H, W, 3), dtype=torch.uint8, device=dev) for _ in range(slots)]
+        self.dout = [torch.empty((chunk, H, W, 3), dtype=torch.uint8, device=dev) for _ in range(slots)]
+        self.dair = [torch.empty((chunk, 3), dtype=torch.float64, device=dev) for _ in range(slots)]
+
+
+_host_pipes: dict = {}
+
+
+def dehaze_host_batch(frames, params=None, out=None, airlight=None, chunk=None):
+    """Dehaze a HOST batch (n, H, W, 3) uint8 torch tensor (pinned for overlap) end to end.
+
+    Frames move to the GPU in chunks on a ring of streams: H2D copy, fused
+    pipeline and D2H copy of chunk c overlap those of chunks c-1 and c+1.
+    Returns (out, airlight) host tensors (pinned when allocated here).
+    Native-size frames only (the resize path is per-frame float64).
+    """
+    import torch
+
+    if params is None:
+        params = DehazeParams()
+    params.validate()
+    n, H, W = int(frames.shape[0]), int(frames.shape[1]), int(frames.shape[2])
+    if _needs_resize(params, H, W):
+        raise ValueError("dehaze_host_batch needs frames at the working size (resize_to None or equal)")
+    dev = _device()
+    if out is None:
+        out = torch.empty((n, H, W, 3), dtype=torch.uint8, pin_memory=True)
+    if airlight is None:
+        airlight = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
+    if n == 0:
+        return out, airlight
+    if chunk is None:
+        chunk = max(1, min(n, (48 << 20) // (3 * H * W)))
+    key = (dev.index, chunk, H, W)
+    pipe = _host_pipes.get(key)
+    if pipe is None:
+        pipe = _host_pipes[key] = _HostPipe(dev, chunk, H, W)
+    cur = torch.cuda.current_stream(dev)
+    for st in pipe.streams:
+        st.wait_stream(cur)
+    for c, lo in enumerate(range(0, n, chunk)):
+        s = c % len(pipe.streams)
+        st = pipe.streams[s]
+        m = min(chunk, n - lo)
+        with torch.cuda.stream(st):
+            pipe.din[s][:m].copy_(frames[lo: lo + m], non_blocking=True)
+            pipe.engines[s].run(pipe.din[s][:m], params, out=pipe.dout[s][:m], airlight=pipe.dair[s][:m],
+                                stream=st)
+            out[lo: lo + m].copy_(pipe.dout[s][:m], non_blocking=True)
+            airlight[lo: lo + m].copy_(pipe.dair[s][:m], non_blocking=True)
+    for st in pipe.streams:
+        st.synchronize()
+    return out, airlight
+
+
+_STREAM_BATCH_BYTES = 256 << 20   # ~256 MiB of input frames per device launch
+_STREAM_BATCH_MAX = 256
+
+
+def process_stream(frames, params=None, sink=None, workers=1):
+    """Run the pipeline over an iterable of uint8 frames, in order (reference pipeline.py:232-308).
+
+    Frames are validated as they arrive and dehazed in device batches; each
+    output frame reaches ``sink`` in input order.  A mid-stream size change
+    raises after every frame before it has been dehazed and handed to the sink.
+    """
+    if params is None:
+        params = DehazeParams()
+    params.validate()
+    workers = int(workers)
+    if workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+
+    trace = []
+    count = 0
+    expected_shape = None
+    start = time.perf_counter()
+    pending = []
+    dev = None
+
+    def flush():
+        nonlocal count
+        if not pending:
+            return
+        batch = _as_device_batch(np.stack(pending), dev)
+        out, air = dehaze_batch(batch, params)
+        out_h = out.cpu().numpy()
+        air_h = air.cpu().numpy()
+        for i in range(len(pending)):
+            if sink is not None:
+                sink(out_h[i])
+            trace.append(air_h[i].copy())
+            count += 1
+        pending.clear()
+
+    for index, frame in enumerate(frames):
+        try:
+            frame = check_u8_frame(frame, name=f"frame {index}")
+            if not isinstance(frame, np.ndarray):
+                frame = frame.cpu().numpy()
+            if expected_shape is None:
+                expected_shape = frame.shape
+                dev = _device()
+                per = frame.nbytes
+                limit = max(1, min(_STREAM_BATCH_MAX, _STREAM_BATCH_BYTES // max(per, 1)))
+            elif frame.shape != expected_shape:
+                raise ValueError(
+                    f"frame {index} has size {frame.shape[1]}x{frame.shape[0]}, "
+                    f"expected {expected_shape[1]}x{expected_shape[0]}"
+                )
+        except ValueError:
+            flush()
+            raise
+        pending.append(frame)
+        if len(pending) >= limit:
+            flush()
+    flush()
+
+    wall = time.perf_counter() - start
+    fps = count / wall if wall > 0 and count else 0.0
+    return StreamStats(frame_count=count, wall_time=wall, fps=fps, airlight_trace=trace)
