@@ -32,7 +32,7 @@ constexpr int64_t kAlign = 256;
 int64_t align_up(int64_t v, int64_t a = kAlign) { return (v + a - 1) / a * a; }
 
 struct Layout {
-  int64_t frame_max, sel, seg_hist, seg_meta, seg_full, sel_idx, lut, dark, tmap, total;
+  int64_t frame_max, sel, row_max, seg_hist, seg_meta, seg_full, sel_idx, lut, dark, tmap, total;
   int64_t dark_fs;
   int S;
 };
@@ -50,6 +50,7 @@ Layout make_layout(int n, int H, int W, const dhz_params* p) {
   };
   L.frame_max = take(4LL * n);
   L.sel = take((int64_t)sizeof(dhz::FrameSel) * n);
+  L.row_max = take(4LL * n * ((H + 15) / 16));
   L.seg_hist = take(4LL * n * L.S * dhz::kWin);
   L.seg_meta = take(16LL * n * L.S);
   L.seg_full = take(1024LL * n * L.S);
@@ -135,18 +136,22 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const d
   };
   mark(0);
   uint8_t* base = static_cast<uint8_t*>(ws);
-  cudaError_t e = cudaMemsetAsync(base, 0, (size_t)L.seg_hist, st);  // frame_max + sel records
+  cudaError_t e = cudaMemsetAsync(base, 0, (size_t)L.seg_hist, st);  // frame_max, sel records, row_max
   if (e != cudaSuccess) return cuda_fail(e, "memset");
 
   uint8_t* dark = base + L.dark;
   uint32_t* fmax = reinterpret_cast<uint32_t*>(base + L.frame_max);
-  e = dhz::dark_u8(in, in_fs, n, H, W, p->patch_radius, dark, L.dark_fs, fmax, st);
+  uint32_t* rmax = reinterpret_cast<uint32_t*>(base + L.row_max);
+  e = dhz::dark_u8(in, in_fs, n, H, W, p->patch_radius, dark, L.dark_fs, fmax, rmax, st);
   if (e != cudaSuccess) return cuda_fail(e, "dark_u8");
   mark(1);
 
   dhz::SelectWs sw{};
   sw.sel = reinterpret_cast<dhz::FrameSel*>(base + L.sel);
   sw.frame_max = fmax;
+  sw.band_max = rmax;
+  sw.H = H;
+  sw.W = W;
   sw.seg_hist = reinterpret_cast<uint32_t*>(base + L.seg_hist);
   sw.seg_full = reinterpret_cast<uint32_t*>(base + L.seg_full);
   sw.seg_meta = reinterpret_cast<uint32_t*>(base + L.seg_meta);

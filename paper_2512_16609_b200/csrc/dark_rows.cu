@@ -1,0 +1,235 @@
+// K1 — dark channel of u8 RGB frames, row-major two-pass kernel (the fast path).
+//
+// Contract (reference estimation.py:35-43, morphology.py:17-73): dark =
+// (2r+1)^2 erosion of the per-pixel channel minimum, window clamped to the
+// image (== replicate padding for a min).  Bit-exact on the u8 grid.
+//
+// Tile: 480 output columns x 64 output rows, 256 threads (8 warps), ~37 KB
+// of shared memory -> 5 CTAs / SM.
+//  pass 1 (warp per row, rows y0-r .. y0+64+r): each lane streams 16 pixels
+//    (3 coalesced 128-bit loads), forms their channel minima on 16-bit lanes,
+//    borrows r pixels from each neighbour lane with shuffles and runs the
+//    horizontal window min in registers (power-of-3 window growth on
+//    VIMNMX3.U16x2, funnel shifts for odd offsets).  Lanes 0 and 31 only
+//    supply halo, so a warp yields 480 pixels; the row goes to shared memory.
+//  pass 2 (thread per 4 columns x 16 rows): vertical window min of the
+//    shared rows in registers and a coalesced 4-byte store per row, plus the
+//    max over each 16-row band (band_max[], frame_max[]) that lets the top-K
+//    select skip bands that cannot hold selected pixels.
+#include "dhz_common.cuh"
+#include "dhz_internal.h"
+
+namespace dhz {
+
+namespace {
+
+constexpr int kTW = 480;   // output columns per tile (30 lanes x 16 px)
+constexpr int kBH = 64;    // output rows per tile
+constexpr int kRun = 16;   // rows per pass-2 item (== band height of band_max)
+constexpr int kThreads = 256;
+
+template <int R>
+struct RowGeo {
+  static constexpr int L = 2 * R + 1;
+  static constexpr int ROWS = kBH + 2 * R;
+  static constexpr int P = L >= 27 ? 27 : (L >= 9 ? 9 : (L >= 3 ? 3 : 1));
+  static constexpr int HPR = (R + 1) / 2;        // neighbour pairs borrowed each side
+  static constexpr int NP = 2 * HPR + 8 + 1;     // local pairs (+1 neutral pad)
+  static constexpr size_t SMEM = (size_t)ROWS * kTW;
+};
+
+template <int NP>
+__device__ __forceinline__ uint32_t at(const uint32_t (&m)[NP], int px) {
+  return (px & 1) ? shift1(m[px >> 1], m[(px >> 1) + 1]) : m[px >> 1];
+}
+
+// channel minimum of 16 pixels (48 bytes in 12 words) as 8 16x2 pairs
+__device__ __forceinline__ void cmin16_pairs(const uint32_t (&w)[12], uint32_t (&c)[8]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t a = w[3 * q], b = w[3 * q + 1], d = w[3 * q + 2];
+    c[2 * q] = min3(__byte_perm(a, 0u, 0x4340), __byte_perm(a, b, 0x0401) & 0x00FF00FFu,
+                    __byte_perm(a, b, 0x0502) & 0x00FF00FFu);
+    c[2 * q + 1] = min3(__byte_perm(b, d, 0x0502) & 0x00FF00FFu, __byte_perm(b, d, 0x0603) & 0x00FF00FFu,
+                        __byte_perm(d, 0u, 0x4340));
+  }
+}
+
+template <int L, int N>
+__device__ __forceinline__ void vert_levels(uint32_t (&v)[N]) {
+  constexpr int P = L >= 27 ? 27 : (L >= 9 ? 9 : (L >= 3 ? 3 : 1));
+  if (P >= 3) {
+#pragma unroll
+    for (int k = 0; k + 2 < N; ++k) v[k] = min3(v[k], v[k + 1], v[k + 2]);
+  }
+  if (P >= 9) {
+#pragma unroll
+    for (int k = 0; k + 6 < N; ++k) v[k] = min3(v[k], v[k + 3], v[k + 6]);
+  }
+  if (P >= 27) {
+#pragma unroll
+    for (int k = 0; k + 18 < N; ++k) v[k] = min3(v[k], v[k + 9], v[k + 18]);
+  }
+}
+template <int L, int N>
+__device__ __forceinline__ uint32_t vert_final(const uint32_t (&v)[N], int j) {
+  constexpr int P = L >= 27 ? 27 : (L >= 9 ? 9 : (L >= 3 ? 3 : 1));
+  if (L == P) return v[j];
+  if (L <= 2 * P) return min2(v[j], v[j + L - P]);
+  return min3(v[j], v[j + P], v[j + L - P]);
+}
+
+template <int R>
+__global__ void __launch_bounds__(kThreads)
+k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t* __restrict__ dark,
+            int64_t dark_fs, uint32_t* __restrict__ frame_max, uint32_t* __restrict__ band_max) {
+  using G = RowGeo<R>;
+  constexpr int L = G::L, P = G::P, HPR = G::HPR, NP = G::NP;
+  extern __shared__ __align__(16) uint8_t hrow[];  // [ROWS][kTW] horizontal minima
+  __shared__ uint32_t run_max[kBH / kRun];
+  const int f = blockIdx.z;
+  const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kBH;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint8_t* frame = in + (int64_t)f * in_fs;
+  if (threadIdx.x < kBH / kRun) run_max[threadIdx.x] = 0;
+
+  // ---------------- pass 1: channel min + horizontal min, warp per row ----------------
+  const int x = x0 - 16 + 16 * lane;  // first pixel of this lane
+  const bool col_ok = x >= 0 && x < W;  // W % 16 == 0: a 16-px unit is fully in or out
+  for (int v = warp; v < G::ROWS; v += kThreads / 32) {
+    const int y = y0 - R + v;
+    uint32_t c[8];
+    if (y >= 0 && y < H && col_ok) {
+      const uint8_t* src = frame + ((int64_t)y * W + x) * 3;
+      const uint4 a = ldg_nc_v4(src), b = ldg_nc_v4(src + 16), d = ldg_nc_v4(src + 32);
+      const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
+      cmin16_pairs(w, c);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] = 0xFFFFFFFFu;
+    }
+    // local pairs: [HPR from the left lane][8 own][HPR from the right lane][pad]
+    uint32_t m[NP];
+#pragma unroll
+    for (int k = 0; k < HPR; ++k) {
+      m[k] = __shfl_up_sync(0xffffffffu, c[8 - HPR + k], 1);
+      m[HPR + 8 + k] = __shfl_down_sync(0xffffffffu, c[k], 1);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[HPR + k] = c[k];
+    m[NP - 1] = 0xFFFFFFFFu;
+    if (P >= 3) {
+#pragma unroll
+      for (int p = 0; p + 1 < NP; ++p) m[p] = min3(m[p], shift1(m[p], m[p + 1]), m[p + 1]);
+    }
+    if (P >= 9) {
+#pragma unroll
+      for (int p = 0; p + 3 < NP; ++p) m[p] = min3(m[p], shift1(m[p + 1], m[p + 2]), m[p + 3]);
+    }
+    if (P >= 27) {
+#pragma unroll
+      for (int p = 0; p + 9 < NP; ++p) m[p] = min3(m[p], shift1(m[p + 4], m[p + 5]), m[p + 9]);
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t pr[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int s = 2 * HPR + 4 * q + 2 * h - R;  // local window start of the pair's lane 0
+        if (L == P) pr[h] = at(m, s);
+        else if (L <= 2 * P) pr[h] = min2(at(m, s), at(m, s + L - P));
+        else pr[h] = min3(at(m, s), at(m, s + P), at(m, s + L - P));
+      }
+      o[q] = pack2(pr[0], pr[1]);
+    }
+    if (lane >= 1 && lane <= 30)
+      *reinterpret_cast<uint4*>(hrow + (size_t)v * kTW + 16 * (lane - 1)) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  __syncthreads();
+
+  // ---------------- pass 2: vertical min, thread per 4 columns x 16 rows ----------------
+  constexpr int NG = kTW / 4;                 // 120 column groups
+  constexpr int N = kRun + 2 * R;
+  uint32_t tmax = 0;
+  for (int it = threadIdx.x; it < NG * (kBH / kRun); it += kThreads) {
+    const int run = it / NG, g = it - run * NG;
+    const int j0 = run * kRun;
+    const int xo = x0 + 4 * g;
+    uint32_t lo[N], hi[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(hrow + (size_t)(j0 + k) * kTW + 4 * g);
+      lo[k] = unpack_lo(w);
+      hi[k] = unpack_hi(w);
+    }
+    vert_levels<L, N>(lo);
+    vert_levels<L, N>(hi);
+    uint32_t mx = 0;
+    if (xo < W) {
+      uint8_t* dst = dark + (int64_t)f * dark_fs + (int64_t)(y0 + j0) * W + xo;
+#pragma unroll
+      for (int j = 0; j < kRun; ++j) {
+        const uint32_t a = vert_final<L, N>(lo, j), b = vert_final<L, N>(hi, j);
+        if (y0 + j0 + j < H) {
+          *reinterpret_cast<uint32_t*>(dst + (int64_t)j * W) = pack2(a, b);
+          mx = max3u(mx, a, b);
+        }
+      }
+    }
+    mx = max(mx & 0xFFFFu, mx >> 16);
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, sh));
+    // a warp's 32 consecutive items may straddle two runs: fold into both
+    if (lane == 0) atomicMax(&run_max[run], mx);
+    const int run_last = (__shfl_sync(0xffffffffu, it, 31)) / NG;
+    if (lane == 31 && run_last != run) atomicMax(&run_max[run_last], mx);
+    tmax = max(tmax, mx);
+  }
+  __syncthreads();
+  if (threadIdx.x < kBH / kRun) {
+    const int band = (y0 / kRun) + threadIdx.x;
+    if (y0 + threadIdx.x * kRun < H) atomicMax(band_max + (int64_t)f * ((H + kRun - 1) / kRun) + band,
+                                               run_max[threadIdx.x]);
+  }
+  if (threadIdx.x == 0) {
+    uint32_t m = 0;
+    for (int i = 0; i < kBH / kRun; ++i) m = max(m, run_max[i]);
+    atomicMax(frame_max + f, m);
+  }
+}
+
+template <int R>
+cudaError_t launch(const uint8_t* in, int64_t in_fs, int n, int H, int W, uint8_t* dark, int64_t dark_fs,
+                   uint32_t* frame_max, uint32_t* band_max, cudaStream_t st) {
+  using G = RowGeo<R>;
+  auto kern = k_dark_rows<R>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+  if (e != cudaSuccess) return e;
+  dim3 grid((W + kTW - 1) / kTW, (H + kBH - 1) / kBH, n);
+  kern<<<grid, kThreads, G::SMEM, st>>>(in, in_fs, H, W, dark, dark_fs, frame_max, band_max);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool dark_rows_supported(int r, int W, int64_t in_fs, int64_t dark_fs, const void* in, const void* dark) {
+  return r >= 1 && r <= 16 && W % 16 == 0 && in_fs % 16 == 0 && dark_fs % 4 == 0 && (uintptr_t)in % 16 == 0 &&
+         (uintptr_t)dark % 4 == 0;
+}
+
+cudaError_t dark_rows(const uint8_t* in, int64_t in_fs, int n, int H, int W, int r, uint8_t* dark,
+                      int64_t dark_fs, uint32_t* frame_max, uint32_t* band_max, cudaStream_t st) {
+  switch (r) {
+#define DHZ_R(k) \
+  case k:        \
+    return launch<k>(in, in_fs, n, H, W, dark, dark_fs, frame_max, band_max, st);
+    DHZ_R(1) DHZ_R(2) DHZ_R(3) DHZ_R(4) DHZ_R(5) DHZ_R(6) DHZ_R(7) DHZ_R(8)
+    DHZ_R(9) DHZ_R(10) DHZ_R(11) DHZ_R(12) DHZ_R(13) DHZ_R(14) DHZ_R(15) DHZ_R(16)
+#undef DHZ_R
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace dhz

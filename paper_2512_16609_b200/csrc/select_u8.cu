@@ -77,9 +77,9 @@ __device__ __forceinline__ bool last_block_of_frame(uint32_t* ticket, int S) {
 
 template <bool VEC>
 __global__ void __launch_bounds__(kT)
-k_window_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_t K, int S,
-              const uint32_t* __restrict__ frame_max, FrameSel* __restrict__ sel,
-              uint32_t* __restrict__ seg_hist, uint32_t* __restrict__ seg_meta) {
+k_window_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_t K, int S, int W,
+              const uint32_t* __restrict__ frame_max, const uint32_t* __restrict__ band_max,
+              FrameSel* __restrict__ sel, uint32_t* __restrict__ seg_hist, uint32_t* __restrict__ seg_meta) {
   __shared__ uint32_t h[kWin];
   const int f = blockIdx.y, s = blockIdx.x;
   if (threadIdx.x < kWin) h[threadIdx.x] = 0;
@@ -90,6 +90,15 @@ k_window_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, in
   const int64_t b0 = (int64_t)s * kSeg;
   const int64_t b1 = min(npx, b0 + kSeg);
   const uint8_t* p = dark + f * dark_fs;
+  // Skip the read when no 16-row band touching this segment reaches the window
+  // (K1's band maxima): most segments of a natural frame.
+  bool hot = false;
+  {
+    const int64_t H = npx / W, nb = (H + 15) / 16;
+    const int64_t blo = (b0 / W) / 16, bhi = ((b1 - 1) / W) / 16;
+    for (int64_t bb = blo + threadIdx.x; bb <= bhi; bb += kT) hot |= band_max[f * nb + bb] >= L;
+  }
+  if (__syncthreads_or(hot)) {
   uint32_t c0 = 0;
   auto word = [&](uint32_t w) {
     if (w == Mw) {
@@ -112,7 +121,14 @@ k_window_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, in
       const int64_t off = b0 + 16 * (j * kT + threadIdx.x);
       if (off + 16 <= b1) {
         const uint4 v = ldg_nc_v4(p + off);
-        word(v.x); word(v.y); word(v.z); word(v.w);
+        // max of the 16 bytes on 16-bit lanes (native VIMNMX3), then the rare
+        // per-word pass only when some byte reaches the window
+        const uint32_t mx = max3u(max3u(unpack_lo(v.x), unpack_hi(v.x), unpack_lo(v.y)),
+                                  max3u(unpack_hi(v.y), unpack_lo(v.z), unpack_hi(v.z)),
+                                  max2(unpack_lo(v.w), unpack_hi(v.w)));
+        if (max(mx & 0xFFFFu, mx >> 16) >= L) {
+          word(v.x); word(v.y); word(v.z); word(v.w);
+        }
       } else {
         for (int64_t q = off; q < b1 && q < off + 16; ++q) byte(p[q]);
       }
@@ -123,6 +139,7 @@ k_window_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, in
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c0 += __shfl_xor_sync(0xffffffffu, c0, o);
   if ((threadIdx.x & 31) == 0 && c0) atomicAdd(&h[0], c0);
+  }
   __syncthreads();
   uint32_t* mine = seg_hist + ((int64_t)f * S + s) * kWin;
   if (threadIdx.x < kWin) mine[threadIdx.x] = h[threadIdx.x];
@@ -353,13 +370,13 @@ cudaError_t select_u8(const uint8_t* dark, int64_t dark_fs, int n, int64_t npx, 
   const bool vec = (npx % 16 == 0) && (dark_fs % 16 == 0) && ((uintptr_t)dark % 16 == 0);
   dim3 grid(ws.S, n);
   if (vec) {
-    k_window_hist<true><<<grid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.S, ws.frame_max, ws.sel, ws.seg_hist,
-                                              ws.seg_meta);
+    k_window_hist<true><<<grid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.S, ws.W, ws.frame_max, ws.band_max,
+                                              ws.sel, ws.seg_hist, ws.seg_meta);
     k_full_hist<true><<<grid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.S, ws.sel, ws.seg_full, ws.seg_meta);
     k_compact<true><<<grid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.S, ws.sel, ws.seg_meta, ws.sel_idx);
   } else {
-    k_window_hist<false><<<grid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.S, ws.frame_max, ws.sel, ws.seg_hist,
-                                               ws.seg_meta);
+    k_window_hist<false><<<grid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.S, ws.W, ws.frame_max, ws.band_max,
+                                               ws.sel, ws.seg_hist, ws.seg_meta);
     k_full_hist<false><<<grid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.S, ws.sel, ws.seg_full, ws.seg_meta);
     k_compact<false><<<grid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.S, ws.sel, ws.seg_meta, ws.sel_idx);
   }
