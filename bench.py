@@ -341,7 +341,7 @@ def main():
             "pipeline_roofline": {"alg_bytes_per_px": ALG_BYTES[cfg], "achieved": round(pipe_gbs, 1),
                                   "frac": round(pipe_gbs / peak, 4),
                                   "stage_ms": {"dark(K1)": round(stage_ms[0], 4),
-                                               "select+airlight(K2-K4)": round(stage_ms[1], 4),
+                                               "select+airlight(K2-K3)": round(stage_ms[1], 4),
                                                "lut(K5)": round(stage_ms[2], 4),
                                                "recover(K6)": round(stage_ms[3], 4)}},
             "gpu_launches": 7 * args.steps,

@@ -32,15 +32,15 @@ constexpr int64_t kAlign = 256;
 int64_t align_up(int64_t v, int64_t a = kAlign) { return (v + a - 1) / a * a; }
 
 struct Layout {
-  int64_t frame_max, sel, row_max, seg_hist, seg_meta, seg_full, sel_idx, lut, dark, tmap, total;
+  // [0, zero_end) is cleared at the start of every call
+  int64_t frame_max, sel, blk_max, row_hist, frame_hist, zero_end;
+  int64_t row_info, sel_idx, lut, dark, tmap, total;
   int64_t dark_fs;
-  int S;
 };
 
 Layout make_layout(int n, int H, int W, const dhz_params* p) {
   Layout L{};
   const int64_t npx = (int64_t)H * W;
-  L.S = (int)((npx + dhz::kSeg - 1) / dhz::kSeg);
   L.dark_fs = align_up(npx, 16);
   int64_t o = 0;
   auto take = [&](int64_t bytes) {
@@ -48,12 +48,14 @@ Layout make_layout(int n, int H, int W, const dhz_params* p) {
     o = align_up(o + bytes);
     return at;
   };
+  const int64_t nb = (H + dhz::kBandH - 1) / dhz::kBandH, ntx = (W + dhz::kBandW - 1) / dhz::kBandW;
   L.frame_max = take(4LL * n);
   L.sel = take((int64_t)sizeof(dhz::FrameSel) * n);
-  L.row_max = take(4LL * n * ((H + 15) / 16));
-  L.seg_hist = take(4LL * n * L.S * dhz::kWin);
-  L.seg_meta = take(16LL * n * L.S);
-  L.seg_full = take(1024LL * n * L.S);
+  L.blk_max = take(4LL * n * nb * ntx);
+  L.row_hist = take(4LL * dhz::kWin * n * H);
+  L.frame_hist = take(4LL * dhz::kWin * n);
+  L.zero_end = o;
+  L.row_info = take(16LL * n * H);
   L.sel_idx = take(4LL * n * std::max<int64_t>(1, p->top_k));
   L.lut = take(3LL * dhz::kTri * n);
   L.dark = take(L.dark_fs * n);
@@ -136,35 +138,32 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const d
   };
   mark(0);
   uint8_t* base = static_cast<uint8_t*>(ws);
-  cudaError_t e = cudaMemsetAsync(base, 0, (size_t)L.seg_hist, st);  // frame_max, sel records, row_max
+  cudaError_t e = cudaMemsetAsync(base, 0, (size_t)L.zero_end, st);  // maxima, select state, histograms
   if (e != cudaSuccess) return cuda_fail(e, "memset");
 
   uint8_t* dark = base + L.dark;
   uint32_t* fmax = reinterpret_cast<uint32_t*>(base + L.frame_max);
-  uint32_t* rmax = reinterpret_cast<uint32_t*>(base + L.row_max);
-  e = dhz::dark_u8(in, in_fs, n, H, W, p->patch_radius, dark, L.dark_fs, fmax, rmax, st);
+  uint32_t* bmax = reinterpret_cast<uint32_t*>(base + L.blk_max);
+  e = dhz::dark_u8(in, in_fs, n, H, W, p->patch_radius, dark, L.dark_fs, fmax, bmax, st);
   if (e != cudaSuccess) return cuda_fail(e, "dark_u8");
   mark(1);
 
   dhz::SelectWs sw{};
   sw.sel = reinterpret_cast<dhz::FrameSel*>(base + L.sel);
   sw.frame_max = fmax;
-  sw.band_max = rmax;
+  sw.blk_max = bmax;
+  sw.row_hist = reinterpret_cast<uint32_t*>(base + L.row_hist);
+  sw.frame_hist = reinterpret_cast<uint32_t*>(base + L.frame_hist);
+  sw.row_info = reinterpret_cast<uint32_t*>(base + L.row_info);
+  sw.sel_idx = reinterpret_cast<uint32_t*>(base + L.sel_idx);
   sw.H = H;
   sw.W = W;
-  sw.seg_hist = reinterpret_cast<uint32_t*>(base + L.seg_hist);
-  sw.seg_full = reinterpret_cast<uint32_t*>(base + L.seg_full);
-  sw.seg_meta = reinterpret_cast<uint32_t*>(base + L.seg_meta);
-  sw.sel_idx = reinterpret_cast<uint32_t*>(base + L.sel_idx);
-  sw.S = L.S;
-  e = dhz::select_u8(dark, L.dark_fs, n, npx, p->top_k, sw, st);
+  e = dhz::select_u8(dark, L.dark_fs, in, in_fs, n, npx, p->top_k, p->alpha, sw, airlight, st);
   if (e != cudaSuccess) return cuda_fail(e, "select_u8");
-  e = dhz::airlight_sum_u8(in, in_fs, n, npx, p->top_k, p->alpha, sw, airlight, st);
-  if (e != cudaSuccess) return cuda_fail(e, "airlight_sum_u8");
   mark(2);
 
   uint8_t* lut = base + L.lut;
-  e = dhz::build_lut_u8(n, airlight, p->omega, p->t_min, p->thresholds, lut, st);
+  e = dhz::build_lut_u8(n, airlight, p->omega, p->t_min, p->thresholds, p->gamma, lut, st);
   if (e != cudaSuccess) return cuda_fail(e, "build_lut_u8");
   mark(3);
   e = dhz::recover_lut_u8(in, in_fs, n, H, W, lut, out, out_fs, st);

@@ -14,7 +14,7 @@
 //    supply halo, so a warp yields 480 pixels; the row goes to shared memory.
 //  pass 2 (thread per 4 columns x 16 rows): vertical window min of the
 //    shared rows in registers and a coalesced 4-byte store per row, plus the
-//    max over each 16-row band (band_max[], frame_max[]) that lets the top-K
+//    max over each 16-row x 480-column block (blk_max[], frame_max[]) that lets the top-K
 //    select skip bands that cannot hold selected pixels.
 #include "dhz_common.cuh"
 #include "dhz_internal.h"
@@ -23,9 +23,9 @@ namespace dhz {
 
 namespace {
 
-constexpr int kTW = 480;   // output columns per tile (30 lanes x 16 px)
+constexpr int kTW = kBandW;  // output columns per tile (30 lanes x 16 px)
 constexpr int kBH = 64;    // output rows per tile
-constexpr int kRun = 16;   // rows per pass-2 item (== band height of band_max)
+constexpr int kRun = kBandH;  // rows per pass-2 item (== block height of blk_max)
 constexpr int kThreads = 256;
 
 template <int R>
@@ -82,7 +82,7 @@ __device__ __forceinline__ uint32_t vert_final(const uint32_t (&v)[N], int j) {
 template <int R>
 __global__ void __launch_bounds__(kThreads)
 k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t* __restrict__ dark,
-            int64_t dark_fs, uint32_t* __restrict__ frame_max, uint32_t* __restrict__ band_max) {
+            int64_t dark_fs, uint32_t* __restrict__ frame_max, uint32_t* __restrict__ blk_max) {
   using G = RowGeo<R>;
   constexpr int L = G::L, P = G::P, HPR = G::HPR, NP = G::NP;
   extern __shared__ __align__(16) uint8_t hrow[];  // [ROWS][kTW] horizontal minima
@@ -180,17 +180,18 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
     mx = max(mx & 0xFFFFu, mx >> 16);
 #pragma unroll
     for (int sh = 16; sh > 0; sh >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, sh));
-    // a warp's 32 consecutive items may straddle two runs: fold into both
-    if (lane == 0) atomicMax(&run_max[run], mx);
-    const int run_last = (__shfl_sync(0xffffffffu, it, 31)) / NG;
-    if (lane == 31 && run_last != run) atomicMax(&run_max[run_last], mx);
+    // a warp's 32 consecutive items may straddle two runs: fold the warp max into both
+    const int run_first = __shfl_sync(0xffffffffu, run, 0);
+    if (lane == 0) atomicMax(&run_max[run_first], mx);
+    if (lane == 31 && run != run_first) atomicMax(&run_max[run], mx);
     tmax = max(tmax, mx);
   }
   __syncthreads();
-  if (threadIdx.x < kBH / kRun) {
+  if (threadIdx.x < kBH / kRun) {  // max per (16-row band, 480-col tile), owned by this CTA
     const int band = (y0 / kRun) + threadIdx.x;
-    if (y0 + threadIdx.x * kRun < H) atomicMax(band_max + (int64_t)f * ((H + kRun - 1) / kRun) + band,
-                                               run_max[threadIdx.x]);
+    if (y0 + threadIdx.x * kRun < H)
+      blk_max[((int64_t)f * ((H + kBandH - 1) / kBandH) + band) * ((W + kBandW - 1) / kBandW) + blockIdx.x] =
+          run_max[threadIdx.x];
   }
   if (threadIdx.x == 0) {
     uint32_t m = 0;
@@ -201,13 +202,13 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
 
 template <int R>
 cudaError_t launch(const uint8_t* in, int64_t in_fs, int n, int H, int W, uint8_t* dark, int64_t dark_fs,
-                   uint32_t* frame_max, uint32_t* band_max, cudaStream_t st) {
+                   uint32_t* frame_max, uint32_t* blk_max, cudaStream_t st) {
   using G = RowGeo<R>;
   auto kern = k_dark_rows<R>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
   if (e != cudaSuccess) return e;
   dim3 grid((W + kTW - 1) / kTW, (H + kBH - 1) / kBH, n);
-  kern<<<grid, kThreads, G::SMEM, st>>>(in, in_fs, H, W, dark, dark_fs, frame_max, band_max);
+  kern<<<grid, kThreads, G::SMEM, st>>>(in, in_fs, H, W, dark, dark_fs, frame_max, blk_max);
   return cudaGetLastError();
 }
 
@@ -219,11 +220,11 @@ bool dark_rows_supported(int r, int W, int64_t in_fs, int64_t dark_fs, const voi
 }
 
 cudaError_t dark_rows(const uint8_t* in, int64_t in_fs, int n, int H, int W, int r, uint8_t* dark,
-                      int64_t dark_fs, uint32_t* frame_max, uint32_t* band_max, cudaStream_t st) {
+                      int64_t dark_fs, uint32_t* frame_max, uint32_t* blk_max, cudaStream_t st) {
   switch (r) {
 #define DHZ_R(k) \
   case k:        \
-    return launch<k>(in, in_fs, n, H, W, dark, dark_fs, frame_max, band_max, st);
+    return launch<k>(in, in_fs, n, H, W, dark, dark_fs, frame_max, blk_max, st);
     DHZ_R(1) DHZ_R(2) DHZ_R(3) DHZ_R(4) DHZ_R(5) DHZ_R(6) DHZ_R(7) DHZ_R(8)
     DHZ_R(9) DHZ_R(10) DHZ_R(11) DHZ_R(12) DHZ_R(13) DHZ_R(14) DHZ_R(15) DHZ_R(16)
 #undef DHZ_R

@@ -241,7 +241,10 @@ k_dark_u8(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r,
     }
     {
       const uint32_t cm = max(max(tmax & 0xFFu, (tmax >> 8) & 0xFFu), max((tmax >> 16) & 0xFFu, tmax >> 24));
-      if (x < W) atomicMax(row_max + (int64_t)f * ((H + 15) / 16) + y / 16, cm);
+      if (x < W)
+        atomicMax(row_max + ((int64_t)f * ((H + kBandH - 1) / kBandH) + y / kBandH) * ((W + kBandW - 1) / kBandW) +
+                      x / kBandW,
+                  cm);
       tmax = vmax4(tmax, tmax_before);
     }
   }

@@ -19,6 +19,10 @@ constexpr int kSeg = 16384;
 // Width of the max-relative window histogram used by the fast select path.
 constexpr int kWin = 16;
 
+// Dark-map blocks whose maxima K1 records for the select pass (16 rows x 480 columns).
+constexpr int kBandH = 16;
+constexpr int kBandW = 480;
+
 __device__ __forceinline__ uint32_t vmin4(uint32_t a, uint32_t b) { return __vminu4(a, b); }
 __device__ __forceinline__ uint32_t vmax4(uint32_t a, uint32_t b) { return __vmaxu4(a, b); }
 

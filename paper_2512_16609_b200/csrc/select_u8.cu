@@ -8,19 +8,20 @@
 //   A = max(alpha * mean(RGB[selected], axis=0), 1e-6)       (:83-84)
 // numpy's axis-0 mean of a (K, 3) array is a sequential row accumulation in
 // the selection order followed by a true division by K; K4 reproduces that
-// chain exactly, so A is bit-identical to the reference.
+// chain exactly, so A is bit-identical to the reference.  When K == n the
+// reference takes arange(n) (:75-76).
 //
-// K2 (k_window_hist): per 16 KB segment of a frame's dark map, a 16-bin
-//   histogram of the levels [max-15, max] (max from K1).  Only words with a
-//   byte >= max-15 touch shared memory, so the pass is a pure 1 B/px stream.
-//   The last segment-block of each frame (threadfence + ticket) finds T and
-//   writes per-segment (above, tie) counts and their exclusive prefixes.
-// K2b (k_full_hist): fallback when the top K pixels span more than 16 levels
-//   below the max (or the frame is degenerate): full 256-bin histograms.
-// K3 (k_compact): blocks whose segment holds selected pixels write their flat
-//   indices, in index order, at the prefix offsets.
-// K4 (k_airlight_sum): one warp per frame gathers the K selected pixels and
-//   lanes 0..2 run the per-channel sequential fp64 sums.
+// K2 (k_level_hist): warp per 16-row x 480-column dark block.  Blocks whose
+//   maximum (recorded by K1) is below max-15 are skipped without reading; the
+//   others count the pixels of each level in [max-15, max] per row (rare
+//   shared atomics), folded into a per-row / per-frame level histogram.
+// K3 (k_threshold): CTA per frame: T = K-th largest level, per-row (above,
+//   tie) counts and their exclusive prefixes over rows (linear index order).
+//   Frames whose top K spans more than 16 levels are redone by K3b
+//   (k_threshold_full, full 256-level histogram; an early exit otherwise).
+// K4 (k_compact_sum): CTA per frame: warps compact the few rows that hold
+//   selected pixels (ballot-free: per-lane counts + warp scan, index order),
+//   then the gather and the three sequential fp64 channel sums.
 #include "dhz_common.cuh"
 #include "dhz_internal.h"
 
@@ -28,365 +29,359 @@ namespace dhz {
 
 namespace {
 
-constexpr int kT = 256;  // threads per select block
+constexpr int kT = 256;
+constexpr int kWarps = kT / 32;
 
-__device__ __forceinline__ uint32_t ldcg_u32(const uint32_t* p) { return __ldcg(p); }
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, int lane, uint32_t* total) {
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  *total = __shfl_sync(0xffffffffu, x, 31);
+  return x - v;
+}
 
-// Exclusive scan over S segments of two counters produced by `get(s, &a, &t)`;
-// writes meta[s] = {a, t, a_prefix, t_prefix}.  Called by a whole block.
+// ---------------------------------------------------------------------------
+// K2: per-row level histogram of the levels [M-15, M]
+// ---------------------------------------------------------------------------
+template <bool VEC>
+__global__ void __launch_bounds__(kT)
+k_level_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int n, int H, int W,
+             const uint32_t* __restrict__ frame_max, const uint32_t* __restrict__ blk_max,
+             uint32_t* __restrict__ row_hist /* [n][H][16] */, uint32_t* __restrict__ frame_hist /* [n][16] */) {
+  __shared__ uint32_t cnt[kWarps][kBandH][kWin];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nb = (H + kBandH - 1) / kBandH, ntx = (W + kBandW - 1) / kBandW;
+  const int64_t items = (int64_t)n * nb * ntx;
+  uint32_t* c = &cnt[wid][0][0];
+  for (int64_t it = (int64_t)blockIdx.x * kWarps + wid; it < items; it += (int64_t)gridDim.x * kWarps) {
+    const int f = (int)(it / ((int64_t)nb * ntx));
+    const int rem = (int)(it - (int64_t)f * nb * ntx);
+    const int b = rem / ntx, tx = rem - b * ntx;
+    const uint32_t M = frame_max[f];
+    const uint32_t L = M >= (uint32_t)(kWin - 1) ? M - (kWin - 1) : 0u;
+    if (blk_max[it] < L) continue;  // warp-uniform: nothing in the window here
+    for (int k = lane; k < kBandH * kWin; k += 32) c[k] = 0;
+    __syncwarp();
+    const int y0 = b * kBandH, x0 = tx * kBandW;
+    const int rows = min(kBandH, H - y0), cols = min(kBandW, W - x0);
+    const uint8_t* base = dark + (int64_t)f * dark_fs + (int64_t)y0 * W + x0;
+    for (int r = 0; r < rows; ++r) {
+      const uint8_t* row = base + (int64_t)r * W;
+      if (VEC) {
+        const int x = 16 * lane;
+        if (x < cols) {
+          const uint4 v = __ldcg(reinterpret_cast<const uint4*>(row + x));
+          const uint32_t mx = max3u(max3u(unpack_lo(v.x), unpack_hi(v.x), unpack_lo(v.y)),
+                                    max3u(unpack_hi(v.y), unpack_lo(v.z), unpack_hi(v.z)),
+                                    max2(unpack_lo(v.w), unpack_hi(v.w)));
+          if (max(mx & 0xFFFFu, mx >> 16) >= L) {
+            const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const uint32_t bv = (ws[q >> 2] >> (8 * (q & 3))) & 0xFFu;
+              if (bv >= L) atomicAdd(&c[r * kWin + (M - bv)], 1u);
+            }
+          }
+        }
+      } else {
+        for (int x = lane; x < cols; x += 32) {
+          const uint32_t bv = row[x];
+          if (bv >= L) atomicAdd(&c[r * kWin + (M - bv)], 1u);
+        }
+      }
+    }
+    __syncwarp();
+    // flush: per-row entries (rows of this block are shared with other column tiles)
+    uint32_t* rh = row_hist + ((int64_t)f * H + y0) * kWin;
+    for (int k = lane; k < rows * kWin; k += 32) {
+      const uint32_t v = c[k];
+      if (v) atomicAdd(rh + k, v);
+    }
+    // per-level totals over the block's rows
+    if (lane < kWin) {
+      uint32_t s = 0;
+      for (int r = 0; r < rows; ++r) s += c[r * kWin + lane];
+      if (s) atomicAdd(frame_hist + (int64_t)f * kWin + lane, s);
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: threshold + per-row (above, tie) counts and exclusive prefixes
+// ---------------------------------------------------------------------------
+// row_info[f][y] = {above, ties, above_prefix, tie_prefix}
 template <typename Get>
-__device__ void scan_segments(int S, uint32_t* meta, Get get) {
+__device__ void scan_rows(int H, uint32_t* info, Get get) {
   __shared__ uint32_t tmp[32];
-  const int cpt = (S + kT - 1) / kT;
-  const int s0 = threadIdx.x * cpt;
+  const int cpt = (H + kT - 1) / kT;
+  const int y0 = threadIdx.x * cpt, y1 = min(H, y0 + cpt);
   uint32_t la = 0, lt = 0;
-  for (int s = s0; s < min(S, s0 + cpt); ++s) {
+  for (int y = y0; y < y1; ++y) {
     uint32_t a, t;
-    get(s, a, t);
+    get(y, a, t);
     la += a;
     lt += t;
   }
-  uint32_t ta, tt;
-  uint32_t pa = block_exclusive_scan(la, tmp, &ta);
-  uint32_t pt = block_exclusive_scan(lt, tmp, &tt);
-  for (int s = s0; s < min(S, s0 + cpt); ++s) {
+  uint32_t pa = block_exclusive_scan(la, tmp, nullptr);
+  uint32_t pt = block_exclusive_scan(lt, tmp, nullptr);
+  for (int y = y0; y < y1; ++y) {
     uint32_t a, t;
-    get(s, a, t);
-    meta[4 * s + 0] = a;
-    meta[4 * s + 1] = t;
-    meta[4 * s + 2] = pa;
-    meta[4 * s + 3] = pt;
+    get(y, a, t);
+    reinterpret_cast<uint4*>(info)[y] = make_uint4(a, t, pa, pt);
     pa += a;
     pt += t;
   }
 }
 
-__device__ __forceinline__ bool last_block_of_frame(uint32_t* ticket, int S) {
-  __shared__ bool is_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint32_t t = atomicAdd(ticket, 1u);
-    is_last = (t == (uint32_t)S - 1u);
-    if (is_last) *ticket = 0u;  // every other block of the frame has arrived
-  }
-  __syncthreads();
-  if (is_last) __threadfence();
-  return is_last;
-}
-
-template <bool VEC>
 __global__ void __launch_bounds__(kT)
-k_window_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_t K, int S, int W,
-              const uint32_t* __restrict__ frame_max, const uint32_t* __restrict__ band_max,
-              FrameSel* __restrict__ sel, uint32_t* __restrict__ seg_hist, uint32_t* __restrict__ seg_meta) {
-  __shared__ uint32_t h[kWin];
-  const int f = blockIdx.y, s = blockIdx.x;
-  if (threadIdx.x < kWin) h[threadIdx.x] = 0;
-  __syncthreads();
-  const uint32_t M = frame_max[f];
-  const uint32_t L = M >= (uint32_t)(kWin - 1) ? M - (kWin - 1) : 0u;
-  const uint32_t Mw = M * 0x01010101u, Lw = L * 0x01010101u;
-  const int64_t b0 = (int64_t)s * kSeg;
-  const int64_t b1 = min(npx, b0 + kSeg);
-  const uint8_t* p = dark + f * dark_fs;
-  // Skip the read when no 16-row band touching this segment reaches the window
-  // (K1's band maxima): most segments of a natural frame.
-  bool hot = false;
-  {
-    const int64_t H = npx / W, nb = (H + 15) / 16;
-    const int64_t blo = (b0 / W) / 16, bhi = ((b1 - 1) / W) / 16;
-    for (int64_t bb = blo + threadIdx.x; bb <= bhi; bb += kT) hot |= band_max[f * nb + bb] >= L;
-  }
-  if (__syncthreads_or(hot)) {
-  uint32_t c0 = 0;
-  auto word = [&](uint32_t w) {
-    if (w == Mw) {
-      c0 += 4;
-    } else if (__vcmpgeu4(w, Lw)) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t b = (w >> (8 * k)) & 0xFFu;
-        if (b >= L) atomicAdd(&h[M - b], 1u);
-      }
-    }
-  };
-  auto byte = [&](uint32_t b) {
-    if (b == M) c0 += 1;
-    else if (b >= L) atomicAdd(&h[M - b], 1u);
-  };
-  if (VEC) {
-#pragma unroll
-    for (int j = 0; j < kSeg / (16 * kT); ++j) {
-      const int64_t off = b0 + 16 * (j * kT + threadIdx.x);
-      if (off + 16 <= b1) {
-        const uint4 v = ldg_nc_v4(p + off);
-        // max of the 16 bytes on 16-bit lanes (native VIMNMX3), then the rare
-        // per-word pass only when some byte reaches the window
-        const uint32_t mx = max3u(max3u(unpack_lo(v.x), unpack_hi(v.x), unpack_lo(v.y)),
-                                  max3u(unpack_hi(v.y), unpack_lo(v.z), unpack_hi(v.z)),
-                                  max2(unpack_lo(v.w), unpack_hi(v.w)));
-        if (max(mx & 0xFFFFu, mx >> 16) >= L) {
-          word(v.x); word(v.y); word(v.z); word(v.w);
-        }
-      } else {
-        for (int64_t q = off; q < b1 && q < off + 16; ++q) byte(p[q]);
-      }
-    }
-  } else {
-    for (int64_t q = b0 + threadIdx.x; q < b1; q += kT) byte(p[q]);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-  if ((threadIdx.x & 31) == 0 && c0) atomicAdd(&h[0], c0);
-  }
-  __syncthreads();
-  uint32_t* mine = seg_hist + ((int64_t)f * S + s) * kWin;
-  if (threadIdx.x < kWin) mine[threadIdx.x] = h[threadIdx.x];
-
-  if (!last_block_of_frame(&sel[f].ticket, S)) return;
-
-  // ---- last block of frame f: threshold and per-segment prefix offsets ----
-  __shared__ uint32_t part[kT / kWin][kWin];
-  __shared__ uint32_t tot[kWin];
-  __shared__ int jstar_s;
-  const uint32_t* fh = seg_hist + (int64_t)f * S * kWin;
-  {
-    const int j = threadIdx.x % kWin, pi = threadIdx.x / kWin;
-    uint32_t acc = 0;
-    for (int ss = pi; ss < S; ss += kT / kWin) acc += ldcg_u32(fh + ss * kWin + j);
-    part[pi][j] = acc;
-  }
-  __syncthreads();
-  if (threadIdx.x < kWin) {
-    uint32_t acc = 0;
-    for (int i = 0; i < kT / kWin; ++i) acc += part[i][threadIdx.x];
-    tot[threadIdx.x] = acc;
-  }
-  __syncthreads();
+k_threshold(int64_t npx, int64_t K, int H, const uint32_t* __restrict__ frame_max,
+            const uint32_t* __restrict__ row_hist, const uint32_t* __restrict__ frame_hist,
+            FrameSel* __restrict__ sel, uint32_t* __restrict__ row_info) {
+  const int f = blockIdx.x;
+  __shared__ int js_s;
   if (threadIdx.x == 0) {
+    const uint32_t M = frame_max[f];
+    uint32_t mode = kSelFast;
     int js = -1;
-    uint32_t mode = kSelFast, above = 0;
+    uint64_t cum = 0;
     if (K >= npx) {
       mode = kSelAll;
     } else {
-      uint64_t cum = 0;
       for (int j = 0; j < kWin && (uint32_t)j <= M; ++j) {
-        if (cum + tot[j] >= (uint64_t)K) { js = j; break; }
-        cum += tot[j];
+        const uint32_t h = frame_hist[(int64_t)f * kWin + j];
+        if (cum + h >= (uint64_t)K) { js = j; break; }
+        cum += h;
       }
-      if (js < 0) {
-        mode = kSelFull;
-      } else {
-        above = (uint32_t)cum;
-        sel[f].T = M - js;
-        sel[f].above = above;
-      }
+      if (js < 0) mode = kSelFull;
     }
     sel[f].mode = mode;
-    jstar_s = (mode == kSelFast) ? js : -1;
+    if (mode == kSelFast) {
+      sel[f].T = M - js;
+      sel[f].above = (uint32_t)cum;
+    }
+    js_s = mode == kSelFast ? js : -1;
   }
   __syncthreads();
-  const int js = jstar_s;
+  const int js = js_s;
   if (js < 0) return;
-  scan_segments(S, seg_meta + (int64_t)f * S * 4, [&](int ss, uint32_t& a, uint32_t& t) {
-    const uint32_t* hh = fh + ss * kWin;
+  const uint32_t* rh = row_hist + (int64_t)f * H * kWin;
+  scan_rows(H, row_info + (int64_t)f * H * 4, [&](int y, uint32_t& a, uint32_t& t) {
+    const uint32_t* h = rh + (int64_t)y * kWin;
     uint32_t acc = 0;
-    for (int j = 0; j < js; ++j) acc += ldcg_u32(hh + j);
+    for (int j = 0; j < js; ++j) acc += h[j];
     a = acc;
-    t = ldcg_u32(hh + js);
+    t = h[js];
   });
 }
 
+// Fallback: the top K pixels span more than kWin levels below the max.
 template <bool VEC>
 __global__ void __launch_bounds__(kT)
-k_full_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_t K, int S,
-            FrameSel* __restrict__ sel, uint32_t* __restrict__ seg_full, uint32_t* __restrict__ seg_meta) {
-  const int f = blockIdx.y, s = blockIdx.x;
-  if (sel[f].mode != kSelFull) return;  // uniform per frame: all blocks of f agree
+k_threshold_full(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_t K, int H, int W,
+                 FrameSel* __restrict__ sel, uint32_t* __restrict__ row_info) {
+  const int f = blockIdx.x;
+  if (sel[f].mode != kSelFull) return;
+  const uint8_t* p = dark + f * dark_fs;
   __shared__ uint32_t h[256];
+  __shared__ uint32_t T_s;
   h[threadIdx.x] = 0;
   __syncthreads();
-  const int64_t b0 = (int64_t)s * kSeg;
-  const int64_t b1 = min(npx, b0 + kSeg);
-  const uint8_t* p = dark + f * dark_fs;
-  for (int64_t q = b0 + threadIdx.x; q < b1; q += kT) atomicAdd(&h[p[q]], 1u);
-  __syncthreads();
-  uint32_t* mine = seg_full + ((int64_t)f * S + s) * 256;
-  mine[threadIdx.x] = h[threadIdx.x];
-
-  if (!last_block_of_frame(&sel[f].ticket2, S)) return;
-
-  const uint32_t* fh = seg_full + (int64_t)f * S * 256;
-  __shared__ uint32_t tot[256];
-  __shared__ int T_s;
-  {
-    uint32_t acc = 0;
-    for (int ss = 0; ss < S; ++ss) acc += ldcg_u32(fh + ss * 256 + threadIdx.x);
-    tot[threadIdx.x] = acc;
-  }
+  for (int64_t q = threadIdx.x; q < npx; q += kT) atomicAdd(&h[p[q]], 1u);
   __syncthreads();
   if (threadIdx.x == 0) {
     uint64_t cum = 0;
     int T = 0;
     for (int v = 255; v >= 0; --v) {
-      if (cum + tot[v] >= (uint64_t)K) { T = v; break; }
-      cum += tot[v];
+      if (cum + h[v] >= (uint64_t)K) { T = v; break; }
+      cum += h[v];
     }
+    T_s = (uint32_t)T;
     sel[f].T = (uint32_t)T;
     sel[f].above = (uint32_t)cum;
-    T_s = T;
+    sel[f].mode = kSelFast;
   }
   __syncthreads();
-  const int T = T_s;
-  scan_segments(S, seg_meta + (int64_t)f * S * 4, [&](int ss, uint32_t& a, uint32_t& t) {
-    const uint32_t* hh = fh + ss * 256;
-    uint32_t acc = 0;
-    for (int v = T + 1; v < 256; ++v) acc += ldcg_u32(hh + v);
-    a = acc;
-    t = ldcg_u32(hh + T);
+  const uint32_t T = T_s;
+  // per-row counts, warp per row, into row_info[.].x/.y, then prefixes
+  uint4* info = reinterpret_cast<uint4*>(row_info + (int64_t)f * H * 4);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int y = wid; y < H; y += kWarps) {
+    uint32_t na = 0, nt = 0;
+    for (int x = lane; x < W; x += 32) {
+      const uint32_t b = p[(int64_t)y * W + x];
+      na += b > T;
+      nt += b == T;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      na += __shfl_xor_sync(0xffffffffu, na, o);
+      nt += __shfl_xor_sync(0xffffffffu, nt, o);
+    }
+    if (lane == 0) info[y] = make_uint4(na, nt, 0u, 0u);
+  }
+  __syncthreads();
+  scan_rows(H, row_info + (int64_t)f * H * 4, [&](int y, uint32_t& a, uint32_t& t) {
+    const uint4 v = info[y];
+    a = v.x;
+    t = v.y;
   });
-  __syncthreads();
-  if (threadIdx.x == 0) sel[f].mode = kSelFast;
 }
 
+// ---------------------------------------------------------------------------
+// K4: ordered compaction of the rows holding selected pixels + sequential sum
+// ---------------------------------------------------------------------------
 template <bool VEC>
-__global__ void __launch_bounds__(kT)
-k_compact(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_t K, int S,
-          const FrameSel* __restrict__ sel, const uint32_t* __restrict__ seg_meta,
-          uint32_t* __restrict__ sel_idx) {
-  const int f = blockIdx.y, s = blockIdx.x;
-  const uint32_t mode = sel[f].mode;
-  if (mode == kSelAll) {  // K == n: the reference takes arange(n) (estimation.py:75-76)
-    uint32_t* out = sel_idx + (int64_t)f * K;
-    for (int64_t q = (int64_t)s * kSeg + threadIdx.x; q < min(npx, (int64_t)(s + 1) * kSeg); q += kT)
-      out[q] = (uint32_t)q;
-    return;
-  }
-  if (mode != kSelFast) return;
-  const uint32_t T = sel[f].T, above = sel[f].above;
-  const uint32_t need = (uint32_t)K - above;
-  const uint32_t* mt = seg_meta + ((int64_t)f * S + s) * 4;
-  const uint32_t na_s = mt[0], nt_s = mt[1], ao = mt[2], to = mt[3];
-  if (na_s == 0 && (nt_s == 0 || to >= need)) return;
-  const int64_t b0 = (int64_t)s * kSeg + 64 * threadIdx.x;
-  const int64_t b1 = min(npx, (int64_t)s * kSeg + kSeg);
-  const uint8_t* p = dark + f * dark_fs;
-  uint32_t w[16];
-  if (VEC && b0 + 64 <= b1) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint4 v = ldg_nc_v4(p + b0 + 16 * j);
-      w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      uint32_t word = 0;
-      for (int k = 0; k < 4; ++k) {
-        const int64_t q = b0 + 4 * j + k;
-        // bytes past the frame end can never be selected: give them 0 and a
-        // level strictly below T by masking below.
-        const uint32_t b = (q < b1) ? p[q] : 0u;
-        word |= b << (8 * k);
+__device__ void compact_row(const uint8_t* __restrict__ row, int W, uint32_t base_idx, uint32_t T, uint32_t above,
+                            uint32_t need, uint32_t ao, uint32_t to, uint32_t* __restrict__ out, int lane) {
+  for (int x0 = 0; x0 < W; x0 += 512) {
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    const int x = x0 + 16 * lane;
+    int nv = 0;
+    if (VEC) {
+      if (x < W) {
+        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(row + x));
+        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+        nv = 16;
       }
-      w[j] = word;
+    } else {
+      nv = max(0, min(16, W - x));
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (q < nv) w[q >> 2] |= (uint32_t)row[x + q] << (8 * (q & 3));
     }
-  }
-  const int nvalid = (int)max((int64_t)0, min((int64_t)64, b1 - b0));
-  uint32_t na = 0, nt = 0;
-  for (int k = 0; k < nvalid; ++k) {
-    const uint32_t b = (w[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-    na += (b > T);
-    nt += (b == T);
-  }
-  __shared__ uint32_t tmp[32];
-  uint32_t pa = block_exclusive_scan(na, tmp, nullptr);
-  uint32_t pt = block_exclusive_scan(nt, tmp, nullptr);
-  if (na == 0 && nt == 0) return;
-  uint32_t* out = sel_idx + (int64_t)f * K;
-  const uint32_t base_idx = (uint32_t)b0;
-  for (int k = 0; k < nvalid; ++k) {
-    const uint32_t b = (w[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-    if (b > T) {
-      out[ao + pa++] = base_idx + k;
-    } else if (b == T) {
-      const uint32_t r = to + pt++;
-      if (r < need) out[above + r] = base_idx + k;
+    uint32_t na = 0, nt = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const uint32_t b = (w[q >> 2] >> (8 * (q & 3))) & 0xFFu;
+      na += (q < nv) && (b > T);
+      nt += (q < nv) && (b == T);
     }
+    uint32_t ta, tt;
+    uint32_t pa = warp_excl_scan(na, lane, &ta);
+    uint32_t pt = warp_excl_scan(nt, lane, &tt);
+    if (na | nt) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const uint32_t b = (w[q >> 2] >> (8 * (q & 3))) & 0xFFu;
+        if (q < nv) {
+          if (b > T) {
+            out[ao + pa++] = base_idx + x + q;
+          } else if (b == T) {
+            const uint32_t r = to + pt++;
+            if (r < need) out[above + r] = base_idx + x + q;
+          }
+        }
+      }
+    }
+    ao += ta;
+    to += tt;
   }
 }
 
-constexpr int kSumWarps = 4;
-constexpr int kChunk = 256;
-
-__global__ void __launch_bounds__(32 * kSumWarps)
-k_airlight_sum(const uint8_t* __restrict__ in, int64_t in_fs, int n, int64_t npx, int64_t K, double alpha,
-               const FrameSel* __restrict__ sel, const uint32_t* __restrict__ sel_idx,
-               double* __restrict__ airlight) {
+__device__ void airlight_sum(const uint8_t* __restrict__ frame, const uint32_t* __restrict__ idx, int64_t K,
+                             bool all, double alpha, double* __restrict__ A) {
+  constexpr int kChunk = 2048;
   __shared__ double tab[256];
-  __shared__ uint32_t buf[kSumWarps][kChunk];
-  for (int v = threadIdx.x; v < 256; v += blockDim.x) tab[v] = __ddiv_rn((double)v, 255.0);
-  __syncthreads();
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int f = blockIdx.x * kSumWarps + wid;
-  if (f >= n) return;
-  const bool all = sel[f].mode == kSelAll;
-  const uint8_t* frame = in + f * in_fs;
-  const uint32_t* idx = sel_idx + (int64_t)f * K;
+  __shared__ uint32_t buf[kChunk];
+  for (int v = threadIdx.x; v < 256; v += kT) tab[v] = __ddiv_rn((double)v, 255.0);
   double acc = 0.0;
-  const int sh = 8 * (lane < 3 ? lane : 0);
+  const int sh = 8 * (threadIdx.x < 3 ? threadIdx.x : 0);
   for (int64_t base = 0; base < K; base += kChunk) {
     const int cnt = (int)min((int64_t)kChunk, K - base);
-    for (int e = lane; e < cnt; e += 32) {
-      const int64_t px = all ? base + e : (int64_t)idx[base + e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt; e += kT) {
+      const int64_t px = all ? base + e : (int64_t)__ldcg(idx + base + e);
       const uint8_t* q = frame + 3 * px;
-      buf[wid][e] = (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16);
+      buf[e] = (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16);
     }
-    __syncwarp();
-    if (lane < 3) {
+    __syncthreads();
+    if (threadIdx.x < 3) {  // lanes 0..2 of warp 0: one sequential chain per channel
       int e = 0;
       for (; e + 8 <= cnt; e += 8) {
         double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = tab[(buf[wid][e + u] >> sh) & 0xFFu];
+        for (int u = 0; u < 8; ++u) v[u] = tab[(buf[e + u] >> sh) & 0xFFu];
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
       }
-      for (; e < cnt; ++e) acc = __dadd_rn(acc, tab[(buf[wid][e] >> sh) & 0xFFu]);
+      for (; e < cnt; ++e) acc = __dadd_rn(acc, tab[(buf[e] >> sh) & 0xFFu]);
     }
-    __syncwarp();
   }
-  if (lane < 3) {
+  if (threadIdx.x < 3) {
     const double mean = __ddiv_rn(acc, (double)K);
-    airlight[3 * f + lane] = fmax(__dmul_rn(alpha, mean), 1e-6);
+    A[threadIdx.x] = fmax(__dmul_rn(alpha, mean), 1e-6);
   }
+}
+
+// Warp per row; a frame's rows are spread over kCompactParts CTAs.
+constexpr int kCompactParts = 8;
+
+template <bool VEC>
+__global__ void __launch_bounds__(kT)
+k_compact(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_t K, int H, int W,
+          const FrameSel* __restrict__ sel, const uint32_t* __restrict__ row_info, uint32_t* __restrict__ sel_idx) {
+  const int f = blockIdx.y, part = blockIdx.x;
+  const uint32_t mode = sel[f].mode;
+  uint32_t* out = sel_idx + (int64_t)f * K;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (mode == kSelAll) {  // K == n: arange(n)
+    for (int64_t q = (int64_t)part * kT + threadIdx.x; q < npx; q += (int64_t)kT * kCompactParts)
+      out[q] = (uint32_t)q;
+    return;
+  }
+  const uint32_t T = sel[f].T, above = sel[f].above;
+  const uint32_t need = (uint32_t)K - above;
+  const uint4* info = reinterpret_cast<const uint4*>(row_info + (int64_t)f * H * 4);
+  const uint8_t* p = dark + f * dark_fs;
+  for (int y = part * kWarps + wid; y < H; y += kWarps * kCompactParts) {
+    const uint4 ri = info[y];  // above, ties, above_prefix, tie_prefix
+    if (ri.x == 0 && (ri.y == 0 || ri.w >= need)) continue;
+    compact_row<VEC>(p + (int64_t)y * W, W, (uint32_t)((int64_t)y * W), T, above, need, ri.z, ri.w, out, lane);
+  }
+}
+
+__global__ void __launch_bounds__(kT)
+k_airlight(const uint8_t* __restrict__ in, int64_t in_fs, int64_t K, double alpha, const FrameSel* __restrict__ sel,
+           const uint32_t* __restrict__ sel_idx, double* __restrict__ airlight) {
+  const int f = blockIdx.x;
+  airlight_sum(in + f * in_fs, sel_idx + (int64_t)f * K, K, sel[f].mode == kSelAll, alpha, airlight + 3 * f);
 }
 
 }  // namespace
 
-cudaError_t select_u8(const uint8_t* dark, int64_t dark_fs, int n, int64_t npx, int64_t K,
-                      const SelectWs& ws, cudaStream_t st) {
-  const bool vec = (npx % 16 == 0) && (dark_fs % 16 == 0) && ((uintptr_t)dark % 16 == 0);
-  dim3 grid(ws.S, n);
-  if (vec) {
-    k_window_hist<true><<<grid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.S, ws.W, ws.frame_max, ws.band_max,
-                                              ws.sel, ws.seg_hist, ws.seg_meta);
-    k_full_hist<true><<<grid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.S, ws.sel, ws.seg_full, ws.seg_meta);
-    k_compact<true><<<grid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.S, ws.sel, ws.seg_meta, ws.sel_idx);
-  } else {
-    k_window_hist<false><<<grid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.S, ws.W, ws.frame_max, ws.band_max,
-                                               ws.sel, ws.seg_hist, ws.seg_meta);
-    k_full_hist<false><<<grid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.S, ws.sel, ws.seg_full, ws.seg_meta);
-    k_compact<false><<<grid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.S, ws.sel, ws.seg_meta, ws.sel_idx);
-  }
-  return cudaGetLastError();
-}
+size_t select_row_hist_bytes(int n, int H) { return 4ull * kWin * (size_t)n * H; }
 
-cudaError_t airlight_sum_u8(const uint8_t* in, int64_t in_fs, int n, int64_t npx, int64_t K, double alpha,
-                            const SelectWs& ws, double* airlight, cudaStream_t st) {
-  const int blocks = (n + kSumWarps - 1) / kSumWarps;
-  k_airlight_sum<<<blocks, 32 * kSumWarps, 0, st>>>(in, in_fs, n, npx, K, alpha, ws.sel, ws.sel_idx, airlight);
+cudaError_t select_u8(const uint8_t* dark, int64_t dark_fs, const uint8_t* in, int64_t in_fs, int n, int64_t npx,
+                      int64_t K, double alpha, const SelectWs& ws, double* airlight, cudaStream_t st) {
+  const int H = ws.H, W = ws.W;
+  const bool vec = (W % 16 == 0) && (dark_fs % 16 == 0) && ((uintptr_t)dark % 16 == 0);
+  const int nb = (H + kBandH - 1) / kBandH, ntx = (W + kBandW - 1) / kBandW;
+  const int64_t items = (int64_t)n * nb * ntx;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int g2 = (int)std::min<int64_t>((items + kWarps - 1) / kWarps, 8LL * sms);
+  if (vec) {
+    k_level_hist<true><<<g2, kT, 0, st>>>(dark, dark_fs, n, H, W, ws.frame_max, ws.blk_max, ws.row_hist,
+                                          ws.frame_hist);
+  } else {
+    k_level_hist<false><<<g2, kT, 0, st>>>(dark, dark_fs, n, H, W, ws.frame_max, ws.blk_max, ws.row_hist,
+                                           ws.frame_hist);
+  }
+  k_threshold<<<n, kT, 0, st>>>(npx, K, H, ws.frame_max, ws.row_hist, ws.frame_hist, ws.sel, ws.row_info);
+  const dim3 cgrid(kCompactParts, n);
+  if (vec) {
+    k_threshold_full<true><<<n, kT, 0, st>>>(dark, dark_fs, npx, K, H, W, ws.sel, ws.row_info);
+    k_compact<true><<<cgrid, kT, 0, st>>>(dark, dark_fs, npx, K, H, W, ws.sel, ws.row_info, ws.sel_idx);
+  } else {
+    k_threshold_full<false><<<n, kT, 0, st>>>(dark, dark_fs, npx, K, H, W, ws.sel, ws.row_info);
+    k_compact<false><<<cgrid, kT, 0, st>>>(dark, dark_fs, npx, K, H, W, ws.sel, ws.row_info, ws.sel_idx);
+  }
+  k_airlight<<<n, kT, 0, st>>>(in, in_fs, K, alpha, ws.sel, ws.sel_idx, airlight);
   return cudaGetLastError();
 }
 
