@@ -57,7 +57,7 @@ Layout make_layout(int n, int H, int W, const dhz_params* p) {
   L.zero_end = o;
   L.row_info = take(16LL * n * H);
   L.sel_idx = take(4LL * n * std::max<int64_t>(1, p->top_k));
-  L.lut = take(3LL * dhz::kTri * n);
+  L.lut = take((int64_t)dhz::kLutFrame * n);
   L.dark = take(L.dark_fs * n);
   L.tmap = -1;
   if (p->mode == 1) L.tmap = take(8LL * npx * n);

@@ -13,8 +13,11 @@ namespace dhz {
 // Number of (i, m) pairs with 0 <= m <= i <= 255: the triangular LUT row size.
 constexpr int kTri = 256 * 257 / 2;  // 32896
 
-// Dark-map segment length (bytes) used by the top-K select kernels.
-constexpr int kSeg = 16384;
+// Per-frame recovery table (K5 writes it, K6 stages it in shared memory): three
+// triangular planes, entry (i, m <= i) of channel c at c*kTri + i*(i+1)/2 + m.
+// (A 260-byte-pitch square layout has ~12% fewer bank conflicts but needs 196 KB,
+// i.e. one CTA per SM, and measured slower than two 99 KB CTAs per SM.)
+constexpr int kLutFrame = 3 * kTri;  // 98688 bytes, 16-byte multiple
 
 // Width of the max-relative window histogram used by the fast select path.
 constexpr int kWin = 16;
