@@ -44,9 +44,9 @@ def gather_airlight_trace(local: torch.Tensor, n_frames: int, group=None) -> tor
     if local.shape != (hi - lo, 3):
         raise ValueError(f"rank {rank} holds {tuple(local.shape)}, expected ({hi - lo}, 3)")
     buf[: hi - lo] = local
-    out = torch.empty((world * cap, 3), dtype=torch.float64, device=local.device)
-    dist.all_gather_into_tensor(out, buf, group=group)
-    parts = [out[r * cap: r * cap + (h - l)] for r, (l, h) in enumerate(sizes)]
+    bufs = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(bufs, buf, group=group)
+    parts = [bufs[r][: h - l] for r, (l, h) in enumerate(sizes)]
     return torch.cat(parts, 0)
 
 

@@ -111,6 +111,39 @@ class FrameEngine:
         return out, airlight
 
 
+class StreamedEngine:
+    """Chunks a device batch over several CUDA streams (one workspace each).
+
+    Consecutive chunks run on different streams, so the dark-channel pass of
+    one chunk (HBM/ALU heavy) overlaps the LUT recovery pass of another
+    (shared-memory bound), and a chunk's frames are still L2-resident when its
+    recovery pass re-reads them.
+    """
+
+    def __init__(self, device, streams=2):
+        self.device = torch.device(device)
+        self.engines = [FrameEngine(self.device) for _ in range(streams)]
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(streams)]
+
+    def run(self, frames, params, out=None, airlight=None, chunk=16):
+        n = frames.shape[0]
+        if out is None:
+            out = torch.empty_like(frames)
+        if airlight is None:
+            airlight = torch.empty((n, 3), dtype=torch.float64, device=frames.device)
+        cur = torch.cuda.current_stream(self.device)
+        for st in self.streams:
+            st.wait_stream(cur)
+        for c, lo in enumerate(range(0, n, chunk)):
+            k = c % len(self.streams)
+            hi = min(n, lo + chunk)
+            self.engines[k].run(frames[lo:hi], params, out=out[lo:hi], airlight=airlight[lo:hi],
+                                stream=self.streams[k])
+        for st in self.streams:
+            cur.wait_stream(st)
+        return out, airlight
+
+
 _engines: dict = {}
 _engines_lock = threading.Lock()
 
