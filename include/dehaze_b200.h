@@ -89,6 +89,52 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int height, int width
  * [4] total workspace bytes. */
 int dhz_frames_u8_layout(int n, int height, int width, const dhz_params* p, int64_t* offsets5);
 
+/* ---------------------------------------------------------------------------
+ * float64 stage operations (reference public functions on float64 arrays; one
+ * numpy operation = one IEEE rounding, so results match numpy bit for bit except
+ * power() and the summation order of means / box sums).  Images are (H, W, 3),
+ * maps (H, W); `n` counts elements, `npx` pixels.  Scratch buffers (`tmp`, `ws`)
+ * are caller-allocated device memory of the stated size.
+ * ------------------------------------------------------------------------- */
+/* validation.py:32-72 helper: out3 = {all finite ? 1 : 0, min, max}; ws >= 3*1024 doubles */
+int dhz_f64_stats(const double* x, int64_t n, double* out3, double* ws, void* stream);
+/* imageops.py:18-21 u8_to_float */
+int dhz_u8_to_f64(const uint8_t* in, int64_t n, double* out, void* stream);
+/* imageops.py:24-36 float_to_u8 (clip, *255, +0.5, floor) */
+int dhz_f64_to_u8(const double* in, int64_t n, uint8_t* out, void* stream);
+/* imageops.py:39-44 to_grayscale */
+int dhz_to_grayscale_f64(const double* img, int64_t npx, double* out, void* stream);
+/* imageops.py:47-78 resize_bilinear; the _u8 variant fuses u8_to_float */
+int dhz_resize_bilinear_f64(const double* in, int h, int w, int height, int width, double* out, void* stream);
+int dhz_resize_bilinear_u8(const uint8_t* in, int h, int w, int height, int width, double* out, void* stream);
+/* estimation.py:35-38 channel_min */
+int dhz_channel_min_f64(const double* img, int64_t npx, double* out, void* stream);
+/* morphology.py:63-73 min_filter (radius >= 1; tmp: H*W doubles) */
+int dhz_min_filter_f64(const double* m, int height, int width, int radius, double* out, double* tmp, void* stream);
+/* estimation.py:110-125 box_filter (radius >= 1; tmp: H*W doubles) */
+int dhz_box_filter_f64(const double* m, int height, int width, int radius, double* out, double* tmp, void* stream);
+/* estimation.py:144-172 guided_filter; floor_t > 0 also applies pipeline.py:203
+ * max(q, t_min); ws: 7*H*W doubles */
+int dhz_guided_filter_f64(const double* p, const double* guide, int height, int width, int radius, double eps,
+                          double floor_t, double* out, double* ws, void* stream);
+/* estimation.py:87-101 transmission_from_channel_min; airlight: 3 doubles (device) */
+int dhz_transmission_f64(const double* cmin, int64_t npx, const double* airlight, double omega, double t_min,
+                         double* out, void* stream);
+/* recover.py:28-43 recover_radiance */
+int dhz_recover_f64(const double* img, const double* airlight, const double* t, int64_t npx, double* out,
+                    void* stream);
+/* recover_radiance -> gamma_correct -> float_to_u8 fused, exact through the threshold table */
+int dhz_recover_quant_f64(const double* img, const double* airlight, const double* t, int64_t npx,
+                          const double* thresholds, uint8_t* out, void* stream);
+/* recover.py:46-54 gamma_correct (gamma != 1; the caller copies for gamma == 1) */
+int dhz_gamma_f64(const double* in, int64_t n, double gamma, double* out, void* stream);
+/* recover.py:57-69 gray_world_balance; ws >= 3*256 + 4 doubles */
+int dhz_gray_world_f64(const double* img, int64_t npx, double* out, double* ws, void* stream);
+/* estimation.py:46-84 estimate_airlight on a float64 dark map: airlight (3 doubles) and the
+ * K selected flat indices in summation order */
+int dhz_airlight_f64(const double* img, const double* dark, int64_t npx, int64_t top_k, double alpha,
+                     double* airlight, uint32_t* selected, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -60,6 +60,27 @@ SIGNATURES = {
     "dhz_frames_u8": (_c_int, [_c_void_p, _c_i64, _c_int, _c_int, _c_int, _P, _c_void_p, _c_i64,
                                _c_void_p, _c_void_p, _c_size, _c_void_p, _c_void_p]),
     "dhz_frames_u8_layout": (_c_int, [_c_int, _c_int, _c_int, _P, ctypes.POINTER(_c_i64)]),
+    # float64 stage operations
+    "dhz_f64_stats": (_c_int, [_c_void_p, _c_i64, _c_void_p, _c_void_p, _c_void_p]),
+    "dhz_u8_to_f64": (_c_int, [_c_void_p, _c_i64, _c_void_p, _c_void_p]),
+    "dhz_f64_to_u8": (_c_int, [_c_void_p, _c_i64, _c_void_p, _c_void_p]),
+    "dhz_to_grayscale_f64": (_c_int, [_c_void_p, _c_i64, _c_void_p, _c_void_p]),
+    "dhz_resize_bilinear_f64": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_void_p, _c_void_p]),
+    "dhz_resize_bilinear_u8": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_void_p, _c_void_p]),
+    "dhz_channel_min_f64": (_c_int, [_c_void_p, _c_i64, _c_void_p, _c_void_p]),
+    "dhz_min_filter_f64": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_void_p, _c_void_p]),
+    "dhz_box_filter_f64": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_void_p, _c_void_p]),
+    "dhz_guided_filter_f64": (_c_int, [_c_void_p, _c_void_p, _c_int, _c_int, _c_int, ctypes.c_double,
+                                       ctypes.c_double, _c_void_p, _c_void_p, _c_void_p]),
+    "dhz_transmission_f64": (_c_int, [_c_void_p, _c_i64, _c_void_p, ctypes.c_double, ctypes.c_double,
+                                      _c_void_p, _c_void_p]),
+    "dhz_recover_f64": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_i64, _c_void_p, _c_void_p]),
+    "dhz_recover_quant_f64": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_i64, _c_void_p, _c_void_p,
+                                       _c_void_p]),
+    "dhz_gamma_f64": (_c_int, [_c_void_p, _c_i64, ctypes.c_double, _c_void_p, _c_void_p]),
+    "dhz_gray_world_f64": (_c_int, [_c_void_p, _c_i64, _c_void_p, _c_void_p, _c_void_p]),
+    "dhz_airlight_f64": (_c_int, [_c_void_p, _c_void_p, _c_i64, _c_i64, ctypes.c_double, _c_void_p, _c_void_p,
+                                  _c_void_p]),
 }
 
 _lock = threading.Lock()

@@ -10,11 +10,11 @@
 #include "dhz_internal.h"
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
 
-int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
-int fail(int code, const char* fmt, ...) {
+namespace dhz {
+int abi_fail(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
@@ -23,10 +23,15 @@ int fail(int code, const char* fmt, ...) {
   g_err = buf;
   return code;
 }
-
-int cuda_fail(cudaError_t e, const char* where) {
-  return fail(DHZ_E_CUDA, "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+int abi_cuda_fail(cudaError_t e, const char* where) {
+  return abi_fail(DHZ_E_CUDA, "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
 }
+}  // namespace dhz
+
+namespace {
+
+#define fail dhz::abi_fail
+inline int cuda_fail(cudaError_t e, const char* where) { return dhz::abi_cuda_fail(e, where); }
 
 constexpr int64_t kAlign = 256;
 int64_t align_up(int64_t v, int64_t a = kAlign) { return (v + a - 1) / a * a; }

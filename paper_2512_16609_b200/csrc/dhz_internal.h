@@ -7,6 +7,10 @@
 
 namespace dhz {
 
+// Set the thread-local message returned by dhz_last_error(); return `code`.
+int abi_fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int abi_cuda_fail(cudaError_t e, const char* where);
+
 // Per-frame top-K selection state, one record per frame in the workspace.
 struct FrameSel {
   uint32_t reserved;

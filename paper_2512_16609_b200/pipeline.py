@@ -183,6 +183,12 @@ def _needs_resize(params, h, w):
     return (int(rw), int(rh)) != (w, h)
 
 
+def _native_ok(params, h, w):
+    """The fused u8 batch pipeline covers video mode at the working size; the
+    resize and guided-filter modes (and gray-world balance) use the float64 path."""
+    return params.mode == "video" and not params.balance_enabled() and not _needs_resize(params, h, w)
+
+
 def _as_device_batch(frames_np, device):
     import torch
 
@@ -234,10 +240,10 @@ def dehaze_frame(frame, params=None, telemetry=None):
     is_tensor = not isinstance(frame, np.ndarray)
     dev = frame.device if is_tensor else _device()
     h, w = int(frame.shape[0]), int(frame.shape[1])
-    if _needs_resize(params, h, w):
+    if not _native_ok(params, h, w):
         from .floatpath import dehaze_float_frame
 
-        out, airlight, maps = dehaze_float_frame(frame if is_tensor else _as_device_batch(frame, dev)[0],
+        out, airlight, maps = dehaze_float_frame(frame if is_tensor else _as_device_batch(frame, dev),
                                                  params, tel)
     else:
         batch = frame[None] if is_tensor else _as_device_batch(frame[None], dev)
@@ -278,7 +284,7 @@ def dehaze_batch(frames, params=None, out=None):
         params = DehazeParams()
     params.validate()
     n, h, w = int(frames.shape[0]), int(frames.shape[1]), int(frames.shape[2])
-    if _needs_resize(params, h, w):
+    if not _native_ok(params, h, w):
         import torch
 
         from .floatpath import dehaze_float_frame
@@ -288,6 +294,10 @@ def dehaze_batch(frames, params=None, out=None):
             o, a, _ = dehaze_float_frame(frames[i], params, None)
             outs.append(o)
             airs.append(a)
+        if n == 0:
+            oh, ow = (h, w) if params.resize_to is None else (int(params.resize_to[1]), int(params.resize_to[0]))
+            return (torch.empty((0, oh, ow, 3), dtype=torch.uint8, device=frames.device),
+                    torch.empty((0, 3), dtype=torch.float64, device=frames.device))
         return torch.stack(outs), torch.stack(airs)
     from .engine import engine_for
 
@@ -326,8 +336,16 @@ def dehaze_host_batch(frames, params=None, out=None, airlight=None, chunk=None):
         params = DehazeParams()
     params.validate()
     n, H, W = int(frames.shape[0]), int(frames.shape[1]), int(frames.shape[2])
-    if _needs_resize(params, H, W):
-        raise ValueError("dehaze_host_batch needs frames at the working size (resize_to None or equal)")
+    if not _native_ok(params, H, W):
+        # resize / image mode / balance: float64 device path, frame by frame
+        o, a = dehaze_batch(frames.to(_device()), params)
+        if out is not None:
+            out.copy_(o)
+            o = out
+        if airlight is not None:
+            airlight.copy_(a)
+            a = airlight
+        return o.cpu() if o.is_cuda else o, a.cpu() if a.is_cuda else a
     dev = _device()
     if out is None:
         out = torch.empty((n, H, W, 3), dtype=torch.uint8, pin_memory=True)
