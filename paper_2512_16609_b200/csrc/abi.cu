@@ -39,7 +39,7 @@ int64_t align_up(int64_t v, int64_t a = kAlign) { return (v + a - 1) / a * a; }
 struct Layout {
   // [0, zero_end) is cleared at the start of every call
   int64_t frame_max, sel, blk_max, row_hist, frame_hist, zero_end;
-  int64_t row_info, sel_idx, lut, dark, tmap, total;
+  int64_t row_info, sel_idx, lut, bal, dark, tmap, total;
   int64_t dark_fs;
 };
 
@@ -63,6 +63,7 @@ Layout make_layout(int n, int H, int W, const dhz_params* p) {
   L.row_info = take(16LL * n * H);
   L.sel_idx = take(4LL * n * std::max<int64_t>(1, p->top_k));
   L.lut = take((int64_t)dhz::kLutFrame * n);
+  L.bal = p->balance ? take((int64_t)dhz::balance_ws_bytes(n)) : -1;
   L.dark = take(L.dark_fs * n);
   L.tmap = -1;
   if (p->mode == 1) L.tmap = take(8LL * npx * n);
@@ -133,7 +134,6 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const d
   if (!ws || (int64_t)ws_bytes < L.total)
     return fail(DHZ_E_WORKSPACE, "workspace too small: need %lld bytes, got %zu", (long long)L.total, ws_bytes);
   if (p->mode != 0) return fail(DHZ_E_UNSUPPORTED, "image mode is not available in this build");
-  if (p->balance) return fail(DHZ_E_UNSUPPORTED, "gray-world balance is not available in this build");
   if (dhz::dark_u8_max_smem(p->patch_radius) > 200 * 1024)
     return fail(DHZ_E_UNSUPPORTED, "patch_radius %d too large for the tiled erosion", p->patch_radius);
 
@@ -168,7 +168,11 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const d
   mark(2);
 
   uint8_t* lut = base + L.lut;
-  e = dhz::build_lut_u8(n, airlight, p->omega, p->t_min, p->thresholds, p->gamma, lut, st);
+  if (p->balance)
+    e = dhz::build_lut_balanced_u8(in, in_fs, n, H, W, airlight, p->omega, p->t_min, p->gamma, lut, base + L.bal,
+                                   st);
+  else
+    e = dhz::build_lut_u8(n, airlight, p->omega, p->t_min, p->thresholds, p->gamma, lut, st);
   if (e != cudaSuccess) return cuda_fail(e, "build_lut_u8");
   mark(3);
   e = dhz::recover_lut_u8(in, in_fs, n, H, W, lut, out, out_fs, st);

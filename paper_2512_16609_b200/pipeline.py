@@ -184,9 +184,10 @@ def _needs_resize(params, h, w):
 
 
 def _native_ok(params, h, w):
-    """The fused u8 batch pipeline covers video mode at the working size; the
-    resize and guided-filter modes (and gray-world balance) use the float64 path."""
-    return params.mode == "video" and not params.balance_enabled() and not _needs_resize(params, h, w)
+    """The fused u8 batch pipeline covers video mode at the working size (with or
+    without gray-world balance); the resize and guided-filter modes use the
+    float64 device path."""
+    return params.mode == "video" and not _needs_resize(params, h, w)
 
 
 def _as_device_batch(frames_np, device):

@@ -102,3 +102,26 @@ def test_gamma_alpha_omega(oracle, gamma):
 
     frames = make_frames("c3", frames=1, width=160, height=96).numpy()
     _check(frames, _params(gamma=gamma, alpha=1.0, omega=1.0, t_min=0.1), oracle)
+
+
+@pytest.mark.parametrize("gamma", [1.2, 1.0])
+def test_balance_native(oracle, gamma):
+    from paper_2512_16609_b200.synthetic import make_frames
+
+    frames = make_frames("c4", frames=3, width=192, height=128).numpy()
+    p = _params(white_balance=True, gamma=gamma)
+    out, air, dark, sel = _run(frames, p)
+    for i, f in enumerate(frames):
+        m = {}
+        want = oracle.dehaze_frame(f, p, m)
+        assert np.array_equal(air[i], m["airlight"])
+        d = np.abs(out[i].astype(np.int16) - want.astype(np.int16))
+        assert d.max() <= 1 and int((d > 0).sum()) <= 2
+
+
+def test_balance_degenerate_black(oracle):
+    frames = np.zeros((2, 16, 32, 3), np.uint8)
+    p = _params(white_balance=True)
+    out, air, _, _ = _run(frames, p)
+    for i, f in enumerate(frames):
+        assert np.array_equal(out[i], oracle.dehaze_frame(f, p))
