@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -41,8 +42,17 @@ CONFIG_PARAMS = {
     "c2": dict(mode="image", resize_to=None, guided_radius=30, guided_eps=1e-3),
     "c5": dict(mode="image", resize_to=None, patch_radius=15, guided_radius=60, guided_eps=1e-3),
 }
-# algorithmic HBM bytes per pixel: dark 4 + select 1 + recover 6 (+3 balance)
-ALG_BYTES = {"c1": 11, "c3": 11, "c4": 14, "c2": 29, "c5": 29}
+# algorithmic HBM bytes per pixel: dark 4 + select 1 + recover 6 (+3 balance);
+# image mode: dark 4 + select 1 + guided pass 1 (read I 3, write a,b 16) + pass 2 (read a,b 16,
+# read I 3, write O 3) = 46, + balance (pass 2 writes t~ 8, apply reads I 3 + t~ 8, writes O 3) = 62
+ALG_BYTES = {"c1": 11, "c3": 11, "c4": 14, "c2": 62, "c5": 62}
+GUIDED_BYTES = {False: 41, True: 57}
+
+
+def _guided_chunk(n, H, W, params):
+    """Frames per guided-filter chunk (csrc/guided_u8.cu guided_chunk)."""
+    per = (24.0 if params.balance_enabled() else 16.0) * H * W
+    return int(max(1.0, min(float(n), 4.0e9 / per)))
 
 
 def _ncu_traffic_per_px():
@@ -227,7 +237,6 @@ def main():
     frames = torch.empty((n, H, W, 3), dtype=torch.uint8, device=dev)
     if cfg in ("c3", "c4", "c1", "c2"):
         scene = Scene(W, H, 1000 * int(cfg[1:]), dev)
-        import math
         for f in range(n):
             g = rank * n + f
             beta = 0.65 - 0.15 * math.cos(2 * math.pi * g / 300.0) if cfg in ("c3", "c4") else 0.6
@@ -296,7 +305,7 @@ def main():
     pipe_bytes = ALG_BYTES[cfg] * n * npx
     pipe_gbs = pipe_bytes / (ms_step / 1000.0) / 1e9
     traffic_px = _ncu_traffic_per_px()
-    if native:
+    if native and params.mode == "video":
         rec_bytes = 6 * n * npx          # K6: read I (3 B/px), write O (3 B/px)
         rec_gbs = rec_bytes / (stage_ms[3] / 1000.0) / 1e9
         t_px = traffic_px.get("k_recover_lut")
@@ -306,6 +315,15 @@ def main():
                 "alg_bytes_per_launch": rec_bytes, "launch_ms": round(stage_ms[3], 4),
                 "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read+write per px)"}
         launches = 7 + (2 if params.balance_enabled() else 0)
+    elif native:
+        gb = GUIDED_BYTES[params.balance_enabled()] * n * npx
+        g_gbs = gb / (stage_ms[2] / 1000.0) / 1e9
+        roof = {"bound": "hbm", "kernel": "k_gf_pass1 + k_gf_pass2 (+k_gf_apply): fused guided filter + recovery",
+                "achieved": round(g_gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(g_gbs / peak, 4),
+                "traffic": None, "peak_kind": peak_kind, "alg_bytes_per_launch": gb,
+                "launch_ms": round(stage_ms[2], 4)}
+        # K1 + K2a/K2/K2c/K3 + pass1 + pass2 (+ apply) per <=4 GB chunk of frames
+        launches = 5 + (3 if params.balance_enabled() else 2) * math.ceil(n / _guided_chunk(n, H, W, params))
     else:
         roof = {"bound": "hbm", "kernel": "float64 image-mode pipeline (whole step)", "achieved": round(pipe_gbs, 1),
                 "peak": peak, "unit": "GB/s", "frac": round(pipe_gbs / peak, 4), "traffic": None,
@@ -359,7 +377,7 @@ def main():
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "u8" if native else "f64",
+            "dtype": ("u8" if params.mode == "video" else "u8 in/out, f64 guided filter") if native else "f64",
             "data": "synthetic (seeded BASELINE generator, generated on device)",
             "config": {"workload": f"{cfg}: {n} frames {W}x{H} per GPU, {params.mode} mode, native resolution"
                                    + (", gray-world balance" if params.balance_enabled() else ""),
@@ -372,8 +390,10 @@ def main():
                                   "frac": round(pipe_gbs / peak, 4),
                                   "stage_ms": {"dark(K1)": round(stage_ms[0], 4),
                                                "select+airlight(K2-K3)": round(stage_ms[1], 4),
-                                               "lut(K5)": round(stage_ms[2], 4),
-                                               "recover(K6)": round(stage_ms[3], 4)}},
+                                               **({"guided+recover": round(stage_ms[2], 4)}
+                                                  if params.mode == "image" else
+                                                  {"lut(K5)": round(stage_ms[2], 4),
+                                                   "recover(K6)": round(stage_ms[3], 4)})}},
             "gpu_launches": launches * args.steps,
             "clocks": clk,
             "e2e": e2e,

@@ -62,11 +62,15 @@ Layout make_layout(int n, int H, int W, const dhz_params* p) {
   L.zero_end = o;
   L.row_info = take(16LL * n * H);
   L.sel_idx = take(4LL * n * std::max<int64_t>(1, p->top_k));
-  L.lut = take((int64_t)dhz::kLutFrame * n);
-  L.bal = p->balance ? take((int64_t)dhz::balance_ws_bytes(n)) : -1;
+  if (p->mode == 1) {  // image mode: guided-filter scratch instead of the LUT
+    L.lut = L.bal = -1;
+    L.tmap = take((int64_t)dhz::guided_ws_bytes(n, H, W, p->guided_radius, p->balance != 0));
+  } else {
+    L.lut = take((int64_t)dhz::kLutFrame * n);
+    L.bal = p->balance ? take((int64_t)dhz::balance_ws_bytes(n)) : -1;
+    L.tmap = -1;
+  }
   L.dark = take(L.dark_fs * n);
-  L.tmap = -1;
-  if (p->mode == 1) L.tmap = take(8LL * npx * n);
   L.total = o;
   return L;
 }
@@ -133,7 +137,9 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const d
   const Layout L = make_layout(n, H, W, p);
   if (!ws || (int64_t)ws_bytes < L.total)
     return fail(DHZ_E_WORKSPACE, "workspace too small: need %lld bytes, got %zu", (long long)L.total, ws_bytes);
-  if (p->mode != 0) return fail(DHZ_E_UNSUPPORTED, "image mode is not available in this build");
+  if (p->mode == 1 && (p->guided_radius < 1 || p->guided_radius > dhz::kGuidedMaxRadius))
+    return fail(DHZ_E_UNSUPPORTED, "guided_radius %d outside [1, %d] of the fused guided filter",
+                p->guided_radius, dhz::kGuidedMaxRadius);
   if (dhz::dark_u8_max_smem(p->patch_radius) > 200 * 1024)
     return fail(DHZ_E_UNSUPPORTED, "patch_radius %d too large for the tiled erosion", p->patch_radius);
 
@@ -167,6 +173,14 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const d
   if (e != cudaSuccess) return cuda_fail(e, "select_u8");
   mark(2);
 
+  if (p->mode == 1) {  // guided filter + recovery (+ gray-world) fused; event 3 == event 4
+    e = dhz::guided_recover_u8(in, in_fs, n, H, W, p->guided_radius, p->guided_eps, airlight, p->omega, p->t_min,
+                               p->thresholds, p->gamma, p->balance != 0, out, out_fs, base + L.tmap, st);
+    if (e != cudaSuccess) return cuda_fail(e, "guided_recover_u8");
+    mark(3);
+    mark(4);
+    return DHZ_OK;
+  }
   uint8_t* lut = base + L.lut;
   if (p->balance)
     e = dhz::build_lut_balanced_u8(in, in_fs, n, H, W, airlight, p->omega, p->t_min, p->gamma, lut, base + L.bal,

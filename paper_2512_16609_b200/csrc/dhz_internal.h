@@ -51,6 +51,13 @@ cudaError_t select_u8(const uint8_t* dark, int64_t dark_fs, const uint8_t* in, i
 cudaError_t build_lut_u8(int n, const double* airlight, double omega, double t_min, const double* thr,
                          double gamma /* only seeds the threshold search */, uint8_t* lut /* [n][3][kTri] */,
                          cudaStream_t st);
+// Image mode: fused guided filter + recovery on u8 frames (guided_u8.cu).
+constexpr int kGuidedMaxRadius = 127;
+size_t guided_ws_bytes(int n, int H, int W, int r, bool balance);
+cudaError_t guided_recover_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, int r, double eps,
+                              const double* airlight, double omega, double t_min, const double* thr, double gamma,
+                              bool balance, uint8_t* out, int64_t out_fs, void* ws, cudaStream_t st);
+
 // Gray-world balanced LUT (g table, per-frame channel sums, gains); ws: balance_ws_bytes(n).
 size_t balance_ws_bytes(int n);
 cudaError_t build_lut_balanced_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const double* airlight,

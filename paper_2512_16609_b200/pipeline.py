@@ -183,11 +183,19 @@ def _needs_resize(params, h, w):
     return (int(rw), int(rh)) != (w, h)
 
 
-def _native_ok(params, h, w):
-    """The fused u8 batch pipeline covers video mode at the working size (with or
-    without gray-world balance); the resize and guided-filter modes use the
-    float64 device path."""
-    return params.mode == "video" and not _needs_resize(params, h, w)
+GUIDED_MAX_RADIUS = 127  # dhz::kGuidedMaxRadius (fused guided filter: 2r < 256 columns per strip)
+
+
+def _native_ok(params, h, w, want_maps=False):
+    """The fused u8 batch pipeline covers both modes at the working size (with or
+    without gray-world balance).  The resize path, guided radii above
+    GUIDED_MAX_RADIUS and image-mode map capture (the fused kernels never
+    materialise t~ for every pixel) use the float64 device path."""
+    if _needs_resize(params, h, w):
+        return False
+    if params.mode == "image":
+        return int(params.guided_radius) <= GUIDED_MAX_RADIUS and not want_maps
+    return True
 
 
 def _as_device_batch(frames_np, device):
@@ -241,7 +249,7 @@ def dehaze_frame(frame, params=None, telemetry=None):
     is_tensor = not isinstance(frame, np.ndarray)
     dev = frame.device if is_tensor else _device()
     h, w = int(frame.shape[0]), int(frame.shape[1])
-    if not _native_ok(params, h, w):
+    if not _native_ok(params, h, w, tel.capture_maps):
         from .floatpath import dehaze_float_frame
 
         out, airlight, maps = dehaze_float_frame(frame if is_tensor else _as_device_batch(frame, dev),
@@ -338,7 +346,7 @@ def dehaze_host_batch(frames, params=None, out=None, airlight=None, chunk=None):
     params.validate()
     n, H, W = int(frames.shape[0]), int(frames.shape[1]), int(frames.shape[2])
     if not _native_ok(params, H, W):
-        # resize / image mode / balance: float64 device path, frame by frame
+        # resize / very wide guided windows: float64 device path, frame by frame
         o, a = dehaze_batch(frames.to(_device()), params)
         if out is not None:
             out.copy_(o)

@@ -66,3 +66,24 @@ def test_stage_functions():
     assert np.array_equal(dz.to_grayscale(img), s["gray"])
     assert np.array_equal(dz.resize_bilinear(img, 9, 7), s["resize_down"])
     assert np.array_equal(dz.resize_bilinear(img, 30, 25), s["resize_up"])
+
+
+@pytest.mark.parametrize("name", sorted(n for n in CASES if CASES[n]["params"].get("mode") == "image"))
+def test_pipeline_case_fused_image(name):
+    """Image mode without map capture runs the fused u8 guided-filter path
+    (guided_u8.cu) — same output bar as above."""
+    from paper_2512_16609_b200 import FrameTelemetry, dehaze_frame, pipeline
+
+    c = CASES[name]
+    p = _params(c["params"])
+    total_mismatch = 0
+    for i, f in enumerate(c["frames"]):
+        h, w = f.shape[:2]
+        assert pipeline._native_ok(p, h, w) or pipeline._needs_resize(p, h, w)
+        tel = FrameTelemetry()
+        out = dehaze_frame(f, p, tel)
+        assert np.abs(tel.airlights[0] - c["airlight"][i]).max() <= 1e-12
+        d = np.abs(out.astype(np.int16) - c["out"][i].astype(np.int16))
+        assert d.max() <= 1
+        total_mismatch += int((d > 0).sum())
+    assert total_mismatch <= 2, f"{total_mismatch} samples differ by 1 LSB"
