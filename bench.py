@@ -322,8 +322,8 @@ def main():
                 "achieved": round(g_gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(g_gbs / peak, 4),
                 "traffic": None, "peak_kind": peak_kind, "alg_bytes_per_launch": gb,
                 "launch_ms": round(stage_ms[2], 4)}
-        # K1 + K2a/K2/K2c/K3 + pass1 + pass2 (+ apply) per <=4 GB chunk of frames
-        launches = 5 + (3 if params.balance_enabled() else 2) * math.ceil(n / _guided_chunk(n, H, W, params))
+        # K1 + K2a/K2/K2c/K3 + pass1 + pass2 (+ thresholds + apply) per <=4 GB chunk of frames
+        launches = 5 + (4 if params.balance_enabled() else 2) * math.ceil(n / _guided_chunk(n, H, W, params))
     else:
         roof = {"bound": "hbm", "kernel": "float64 image-mode pipeline (whole step)", "achieved": round(pipe_gbs, 1),
                 "peak": peak, "unit": "GB/s", "frac": round(pipe_gbs / peak, 4), "traffic": None,

@@ -52,7 +52,7 @@ cudaError_t build_lut_u8(int n, const double* airlight, double omega, double t_m
                          double gamma /* only seeds the threshold search */, uint8_t* lut /* [n][3][kTri] */,
                          cudaStream_t st);
 // Image mode: fused guided filter + recovery on u8 frames (guided_u8.cu).
-constexpr int kGuidedMaxRadius = 127;
+constexpr int kGuidedMaxRadius = 255;  // 2r < 512 columns of the wide strip
 size_t guided_ws_bytes(int n, int H, int W, int r, bool balance);
 cudaError_t guided_recover_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, int r, double eps,
                               const double* airlight, double omega, double t_min, const double* thr, double gamma,

@@ -11,14 +11,17 @@
 //   out_c = float_to_u8(gamma(clip((I_c' - A_c) / t~ + A_c)))  [* gray-world gains]
 //
 // Box sums (replicate border == clamped indices, divisor (2r+1)^2 like the
-// reference's SAT) run as column-strip sliding sums: a CTA owns 256 input
-// columns (256-2r output columns) and a segment of rows; each thread keeps the
-// vertical window sums of its column in fp64 registers (add the entering row,
-// drop the leaving one), and every output row takes its horizontal windows from
-// a shared-memory fp64 prefix sum over the 256 columns.  Pass 1 writes a, b
-// (fp64, 16 B/px); pass 2 boxes them, forms t~ and recovers the output bytes
-// directly (exact thresholds), or — with gray-world balance — writes t~ and
-// per-CTA channel sums of the gamma values for the apply pass.
+// reference's SAT) run as column-strip sliding sums: a CTA of 256 threads owns
+// 256*CPT input columns (CPT = 1 or 2 consecutive columns per thread; 256*CPT-2r
+// output columns) and a segment of rows; each thread keeps the vertical window
+// sums of its columns in fp64 registers (add the entering row, drop the leaving
+// one), and every output row takes its horizontal windows from a shared-memory
+// fp64 prefix sum over the strip (thread-local sums + warp scan + warp carries).
+// Pass 1 writes a, b (fp64, 16 B/px); pass 2 boxes them, forms t~ and recovers
+// the output bytes directly (exact thresholds), or — with gray-world balance —
+// writes t~ and per-CTA channel sums of the gamma values; the balance pass then
+// derives per-frame gains and exact per-channel byte thresholds (k_gf_thresholds)
+// and k_gf_apply only recovers and thresholds (no pow per pixel).
 #include <algorithm>
 
 #include "dhz_common.cuh"
@@ -28,140 +31,206 @@ namespace dhz {
 
 namespace {
 
-constexpr int kCols = 256;   // input columns per CTA (one per thread)
+constexpr int kThreads = 256;  // threads per CTA
 
 __device__ __forceinline__ double u8f(uint32_t v) { return __ddiv_rn((double)v, 255.0); }
 
 // Correctly rounded a / b from rb = RN(1/b): q0 = RN(a*rb) lies within 1 ulp of
 // a/b, the FMA residual a - b*q0 is exact, and one correction step rounds to
-// RN(a/b) (Markstein's theorem; b here is a positive normal constant).
+// RN(a/b) (Markstein's theorem; b is a positive normal number here).
 __device__ __forceinline__ double div_rb(double a, double b, double rb) {
   const double q = __dmul_rn(a, rb);
   const double r = __fma_rn(-q, b, a);
   return __fma_rn(r, rb, q);
 }
 
+// x^e for x in [0, 1], e > 0, to a few ulp (exp(e*log(x)) with a 2*atanh
+// series for the log and a degree-13 Taylor exp) — used only inside the
+// gray-world channel sums, where per-sample errors of ~1e-16 are far below the
+// reference's own summation rounding.  Bytes are never derived from it.
+__device__ __forceinline__ double pow_unit(double x, double e) {
+  if (!(x > 0.0)) return 0.0;
+  if (x >= 1.0) return 1.0;
+  int ex;
+  double m = frexp(x, &ex);                 // x = m * 2^ex, m in [0.5, 1)
+  if (m < 0.70710678118654752) { m = m * 2.0; ex -= 1; }   // m in [sqrt(1/2), sqrt(2))
+  const double s = __ddiv_rn(m - 1.0, m + 1.0);
+  const double s2 = s * s;
+  double p = 1.0 / 23;
+  p = fma(p, s2, 1.0 / 21); p = fma(p, s2, 1.0 / 19); p = fma(p, s2, 1.0 / 17); p = fma(p, s2, 1.0 / 15);
+  p = fma(p, s2, 1.0 / 13); p = fma(p, s2, 1.0 / 11); p = fma(p, s2, 1.0 / 9);  p = fma(p, s2, 1.0 / 7);
+  p = fma(p, s2, 1.0 / 5);  p = fma(p, s2, 1.0 / 3);
+  const double lnm = 2.0 * fma(p * s2, s, s);  // 2 atanh(s) = ln(m)
+  constexpr double kLn2Hi = 6.93147180369123816490e-01, kLn2Lo = 1.90821492927058770002e-10;
+  const double y = e * fma((double)ex, kLn2Hi, fma((double)ex, kLn2Lo, lnm));   // e * ln(x) <= 0
+  if (y < -700.0) return 0.0;
+  const double k = rint(y * 1.44269504088896340736);
+  const double r = fma(-k, kLn2Lo, fma(-k, kLn2Hi, y));  // |r| <= ~0.35
+  double q = 1.0 / 6227020800.0;                          // 1/13!
+  q = fma(q, r, 1.0 / 479001600.0); q = fma(q, r, 1.0 / 39916800.0); q = fma(q, r, 1.0 / 3628800.0);
+  q = fma(q, r, 1.0 / 362880.0);    q = fma(q, r, 1.0 / 40320.0);    q = fma(q, r, 1.0 / 5040.0);
+  q = fma(q, r, 1.0 / 720.0);       q = fma(q, r, 1.0 / 120.0);      q = fma(q, r, 1.0 / 24.0);
+  q = fma(q, r, 1.0 / 6.0);         q = fma(q, r, 0.5);              q = fma(q, r, 1.0);
+  q = fma(q, r, 1.0);
+  return ldexp(q, (int)k);
+}
+
 // Per-CTA tables: exact u8 -> fp64 products used by the guide and the coarse t.
 struct GuideTables {
   double wr[256], wg[256], wb[256];  // 0.299*(v/255), 0.587*(v/255), 0.114*(v/255), one rounding each
-  double t[256];                     // clip(1 - omega*((v/255)/max(A)), t_min, 1)
+  double t[256];                     // pass 1: clip(1 - omega*((v/255)/max(A)), t_min, 1); pass 2: v/255
 };
 
-__device__ __forceinline__ void load_tables(GuideTables& T, const double* airlight, int f, double omega,
-                                            double t_min) {
-  const double amax = fmax(fmax(airlight[3 * f], airlight[3 * f + 1]), airlight[3 * f + 2]);
-  for (int v = threadIdx.x; v < 256; v += blockDim.x) {
-    const double x = u8f(v);
-    T.wr[v] = __dmul_rn(0.299, x);
-    T.wg[v] = __dmul_rn(0.587, x);
-    T.wb[v] = __dmul_rn(0.114, x);
-    T.t[v] = fmin(fmax(__dsub_rn(1.0, __dmul_rn(omega, __ddiv_rn(x, amax))), t_min), 1.0);
-  }
+__device__ __forceinline__ void load_guide(GuideTables& T, int v, double x) {
+  T.wr[v] = __dmul_rn(0.299, x);
+  T.wg[v] = __dmul_rn(0.587, x);
+  T.wb[v] = __dmul_rn(0.114, x);
 }
 
 __device__ __forceinline__ double guide_t(const GuideTables& T, uint32_t r, uint32_t g, uint32_t b) {
   return fmin(fmax(__dadd_rn(__dadd_rn(T.wr[r], T.wg[g]), T.wb[b]), 0.0), 1.0);
 }
 
-// Warp-inclusive scan of NQ values, then the cross-warp carry from `wt` (one
-// barrier); returns the CTA-inclusive prefix in v[].
+// tot[q] (this thread's sum over its columns) -> the CTA-exclusive prefix before
+// this thread (warp shuffle scan + carries of the preceding warps; one barrier).
 template <int NQ>
-__device__ __forceinline__ void cta_prefix(double (&v)[NQ], double (*wt)[kCols / 32]) {
+__device__ __forceinline__ void thread_offsets(double (&tot)[NQ], double (*wt)[kThreads / 32]) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double inc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) inc[q] = tot[q];
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      const double y = __shfl_up_sync(0xffffffffu, v[q], o);
-      if (lane >= o) v[q] = __dadd_rn(v[q], y);
+      const double y = __shfl_up_sync(0xffffffffu, inc[q], o);
+      if (lane >= o) inc[q] = __dadd_rn(inc[q], y);
     }
   }
   if (lane == 31) {
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) wt[q][wid] = v[q];
+    for (int q = 0; q < NQ; ++q) wt[q][wid] = inc[q];
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const double ex = __shfl_up_sync(0xffffffffu, inc[q], 1);
+    tot[q] = lane == 0 ? 0.0 : ex;
   }
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     double base = 0.0;
     for (int w = 0; w < wid; ++w) base = __dadd_rn(base, wt[q][w]);
-    v[q] = __dadd_rn(base, v[q]);
+    tot[q] = __dadd_rn(base, tot[q]);
   }
 }
 
 // ---------------------------------------------------------------- pass 1 ----
-// a, b for every pixel of the strip x in [x0, x0 + 256 - 2r), rows [y0, y0 + seg).
-__global__ void __launch_bounds__(kCols)
+// a, b for every pixel of the strip x in [x0, x0 + 256*CPT - 2r), rows [y0, y0 + seg).
+template <int CPT>
+__global__ void __launch_bounds__(kThreads)
 k_gf_pass1(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, int seg, double eps,
            const double* __restrict__ airlight, double omega, double t_min, double* __restrict__ a_out,
            double* __restrict__ b_out) {
+  constexpr int NC = kThreads * CPT;
   __shared__ GuideTables T;
-  __shared__ double pre[2][4][kCols + 1];
-  __shared__ double wt[2][4][kCols / 32];
+  __shared__ double pre[2][4][NC + 1];
+  __shared__ double wt[2][4][kThreads / 32];
   const int f = blockIdx.z;
-  const int sw = kCols - 2 * r;                  // output columns of this strip
+  const int sw = NC - 2 * r;                     // output columns of this strip
   const int x0 = blockIdx.x * sw;                // first output column
   const int y0 = blockIdx.y * seg;
   const int y1 = min(H, y0 + seg);
-  load_tables(T, airlight, f, omega, t_min);
+  {
+    const double amax = fmax(fmax(airlight[3 * f], airlight[3 * f + 1]), airlight[3 * f + 2]);
+    const int v = threadIdx.x;
+    const double x = u8f(v);
+    load_guide(T, v, x);
+    T.t[v] = fmin(fmax(__dsub_rn(1.0, __dmul_rn(omega, __ddiv_rn(x, amax))), t_min), 1.0);
+  }
   if (threadIdx.x < 8) pre[threadIdx.x >> 2][threadIdx.x & 3][0] = 0.0;
   __syncthreads();
-  const int xc = min(max(x0 - r + (int)threadIdx.x, 0), W - 1);  // this thread's (clamped) input column
-  const uint8_t* col = in + (int64_t)f * in_fs + 3LL * xc;
+  const uint8_t* frame = in + (int64_t)f * in_fs;
   const int64_t pitch = 3LL * W;
-  auto feat = [&](int y, double& g, double& p) {
-    const uint8_t* px = col + (int64_t)min(max(y, 0), H - 1) * pitch;
+  int xc[CPT];
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) xc[k] = 3 * min(max(x0 - r + (int)threadIdx.x * CPT + k, 0), W - 1);
+  double s[4][CPT];
+  auto feat = [&](int y, int k, double& g, double& p) {
+    const uint8_t* px = frame + (int64_t)min(max(y, 0), H - 1) * pitch + xc[k];
     const uint32_t R = px[0], G = px[1], B = px[2];
     g = guide_t(T, R, G, B);
     p = T.t[min(min(R, G), B)];
   };
   // vertical window sums for output row y0: rows y0-r .. y0+r (clamped)
-  double sg = 0.0, sp = 0.0, sgp = 0.0, sgg = 0.0;
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) s[0][k] = s[1][k] = s[2][k] = s[3][k] = 0.0;
   for (int d = -r; d <= r; ++d) {
-    double g, p;
-    feat(y0 + d, g, p);
-    sg = __dadd_rn(sg, g);
-    sp = __dadd_rn(sp, p);
-    sgp = __dadd_rn(sgp, __dmul_rn(g, p));
-    sgg = __dadd_rn(sgg, __dmul_rn(g, g));
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      double g, p;
+      feat(y0 + d, k, g, p);
+      s[0][k] = __dadd_rn(s[0][k], g);
+      s[1][k] = __dadd_rn(s[1][k], p);
+      s[2][k] = __dadd_rn(s[2][k], __dmul_rn(g, p));
+      s[3][k] = __dadd_rn(s[3][k], __dmul_rn(g, g));
+    }
   }
   const double kk = (double)(2 * r + 1) * (double)(2 * r + 1);
   const double rkk = __drcp_rn(kk);
-  const int j = (int)threadIdx.x - r;  // output column index within the strip (valid if 0 <= j < sw)
-  const int xo = x0 + j;
-  const bool active = j >= 0 && j < sw && xo < W;
-  const int hi = j + 2 * r + 1, lo = j;
   int buf = 0;
   for (int y = y0; y < y1; ++y, buf ^= 1) {
     if (y > y0) {
-      double g, p, g2, p2;
-      feat(y + r, g, p);
-      feat(y - r - 1, g2, p2);
-      sg = __dsub_rn(__dadd_rn(sg, g), g2);
-      sp = __dsub_rn(__dadd_rn(sp, p), p2);
-      sgp = __dsub_rn(__dadd_rn(sgp, __dmul_rn(g, p)), __dmul_rn(g2, p2));
-      sgg = __dsub_rn(__dadd_rn(sgg, __dmul_rn(g, g)), __dmul_rn(g2, g2));
-    }
-    double v[4] = {sg, sp, sgp, sgg};
-    cta_prefix<4>(v, wt[buf]);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) pre[buf][q][threadIdx.x + 1] = v[q];
-    __syncthreads();
-    if (active) {
-      // window over input columns [j, j + 2r] of the strip = prefix[j+2r+1] - prefix[j]
-      const double mi = div_rb(__dsub_rn(pre[buf][0][hi], pre[buf][0][lo]), kk, rkk);
-      const double mp = div_rb(__dsub_rn(pre[buf][1][hi], pre[buf][1][lo]), kk, rkk);
-      const double cip = div_rb(__dsub_rn(pre[buf][2][hi], pre[buf][2][lo]), kk, rkk);
-      const double cii = div_rb(__dsub_rn(pre[buf][3][hi], pre[buf][3][lo]), kk, rkk);
-      const double var = __dsub_rn(cii, __dmul_rn(mi, mi));
-      const double cov = __dsub_rn(cip, __dmul_rn(mi, mp));
-      const double av = __ddiv_rn(cov, __dadd_rn(var, eps));
-      const int64_t o = (int64_t)f * H * W + (int64_t)y * W + xo;
-      a_out[o] = av;
-      b_out[o] = __dsub_rn(mp, __dmul_rn(av, mi));
+      for (int k = 0; k < CPT; ++k) {
+        double g, p, g2, p2;
+        feat(y + r, k, g, p);
+        feat(y - r - 1, k, g2, p2);
+        s[0][k] = __dsub_rn(__dadd_rn(s[0][k], g), g2);
+        s[1][k] = __dsub_rn(__dadd_rn(s[1][k], p), p2);
+        s[2][k] = __dsub_rn(__dadd_rn(s[2][k], __dmul_rn(g, p)), __dmul_rn(g2, p2));
+        s[3][k] = __dsub_rn(__dadd_rn(s[3][k], __dmul_rn(g, g)), __dmul_rn(g2, g2));
+      }
     }
-    // no trailing barrier: the next row uses the other pre/wt buffer, and the
-    // barrier inside its cta_prefix orders this row's reads before buf is reused
+    double off[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      off[q] = s[q][0];
+#pragma unroll
+      for (int k = 1; k < CPT; ++k) off[q] = __dadd_rn(off[q], s[q][k]);
+    }
+    thread_offsets<4>(off, wt[buf]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double run = off[q];
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        run = __dadd_rn(run, s[q][k]);
+        pre[buf][q][threadIdx.x * CPT + k + 1] = run;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      // output column j of the strip (interleaved over threads: conflict-free reads)
+      const int j = k * kThreads + (int)threadIdx.x;
+      if (j < sw && x0 + j < W) {
+        // window over strip input columns [j, j + 2r] = prefix[j+2r+1] - prefix[j]
+        const int hi = j + 2 * r + 1;
+        const double mi = div_rb(__dsub_rn(pre[buf][0][hi], pre[buf][0][j]), kk, rkk);
+        const double mp = div_rb(__dsub_rn(pre[buf][1][hi], pre[buf][1][j]), kk, rkk);
+        const double cip = div_rb(__dsub_rn(pre[buf][2][hi], pre[buf][2][j]), kk, rkk);
+        const double cii = div_rb(__dsub_rn(pre[buf][3][hi], pre[buf][3][j]), kk, rkk);
+        const double var = __dsub_rn(cii, __dmul_rn(mi, mi));
+        const double cov = __dsub_rn(cip, __dmul_rn(mi, mp));
+        const double av = __ddiv_rn(cov, __dadd_rn(var, eps));
+        const int64_t o = (int64_t)f * H * W + (int64_t)y * W + x0 + j;
+        a_out[o] = av;
+        b_out[o] = __dsub_rn(mp, __dmul_rn(av, mi));
+      }
+    }
+    // no trailing barrier: the next row uses the other pre/wt buffers, and the
+    // barrier inside its thread_offsets orders this row's reads before reuse
   }
 }
 
@@ -173,97 +242,113 @@ __device__ __forceinline__ double recover_x(double x, double A, double t, double
 
 // MODE 0: write output bytes (no balance).  MODE 1: write t~ and per-CTA channel
 // sums of the gamma values (gray-world balance follows in k_gf_apply).
-template <int MODE>
-__global__ void __launch_bounds__(kCols)
+template <int MODE, int CPT>
+__global__ void __launch_bounds__(kThreads)
 k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, int seg,
            const double* __restrict__ a_in,
            const double* __restrict__ b_in, const double* __restrict__ airlight, double t_min,
            const double* __restrict__ thr, double inv_gamma, int gamma_is_one, uint8_t* __restrict__ out,
            int64_t out_fs, double* __restrict__ t_out, double* __restrict__ part) {
+  constexpr int NC = kThreads * CPT;
   __shared__ GuideTables T;  // wr/wg/wb for the guide; t[] holds v/255 here
   __shared__ double sA[3], s_thr[256];
-  __shared__ double pre[2][2][kCols + 1];
-  __shared__ double wt[2][2][kCols / 32];
+  __shared__ double pre[2][2][NC + 1];
+  __shared__ double wt[2][2][kThreads / 32];
   const int f = blockIdx.z;
-  const int sw = kCols - 2 * r;
+  const int sw = NC - 2 * r;
   const int x0 = blockIdx.x * sw;
   const int y0 = blockIdx.y * seg;
   const int y1 = min(H, y0 + seg);
   {
     const int v = threadIdx.x;
     const double x = u8f(v);
-    T.wr[v] = __dmul_rn(0.299, x);
-    T.wg[v] = __dmul_rn(0.587, x);
-    T.wb[v] = __dmul_rn(0.114, x);
+    load_guide(T, v, x);
     T.t[v] = x;
     s_thr[v] = thr[v];
   }
   if (threadIdx.x < 3) sA[threadIdx.x] = airlight[3 * f + threadIdx.x];
   if (threadIdx.x < 4) pre[threadIdx.x >> 1][threadIdx.x & 1][0] = 0.0;
   __syncthreads();
-  const int xc = min(max(x0 - r + (int)threadIdx.x, 0), W - 1);
+  int xc[CPT];
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) xc[k] = min(max(x0 - r + (int)threadIdx.x * CPT + k, 0), W - 1);
   const int64_t fo = (int64_t)f * H * W;
-  auto ab = [&](int y, double& a, double& b) {
-    const int64_t o = fo + (int64_t)min(max(y, 0), H - 1) * W + xc;
-    a = a_in[o];
-    b = b_in[o];
-  };
-  double sa = 0.0, sb = 0.0;
+  double sa[CPT], sb[CPT];
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) sa[k] = sb[k] = 0.0;
   for (int d = -r; d <= r; ++d) {
-    double a, b;
-    ab(y0 + d, a, b);
-    sa = __dadd_rn(sa, a);
-    sb = __dadd_rn(sb, b);
+    const int64_t row = fo + (int64_t)min(max(y0 + d, 0), H - 1) * W;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      sa[k] = __dadd_rn(sa[k], a_in[row + xc[k]]);
+      sb[k] = __dadd_rn(sb[k], b_in[row + xc[k]]);
+    }
   }
   const double kk = (double)(2 * r + 1) * (double)(2 * r + 1);
   const double rkk = __drcp_rn(kk);
-  const int j = (int)threadIdx.x - r;
-  const int xo = x0 + j;
-  const bool active = j >= 0 && j < sw && xo < W;
-  const int hi = j + 2 * r + 1, lo = j;
   const uint8_t* frame = in + (int64_t)f * in_fs;
   const double A0 = sA[0], A1 = sA[1], A2 = sA[2];
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
   int buf = 0;
   for (int y = y0; y < y1; ++y, buf ^= 1) {
     if (y > y0) {
-      double a, b, a2, b2;
-      ab(y + r, a, b);
-      ab(y - r - 1, a2, b2);
-      sa = __dsub_rn(__dadd_rn(sa, a), a2);
-      sb = __dsub_rn(__dadd_rn(sb, b), b2);
+      const int64_t rin = fo + (int64_t)min(y + r, H - 1) * W, rout = fo + (int64_t)max(y - r - 1, 0) * W;
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        sa[k] = __dsub_rn(__dadd_rn(sa[k], a_in[rin + xc[k]]), a_in[rout + xc[k]]);
+        sb[k] = __dsub_rn(__dadd_rn(sb[k], b_in[rin + xc[k]]), b_in[rout + xc[k]]);
+      }
     }
-    double v[2] = {sa, sb};
-    cta_prefix<2>(v, wt[buf]);
-    pre[buf][0][threadIdx.x + 1] = v[0];
-    pre[buf][1][threadIdx.x + 1] = v[1];
+    double off[2] = {sa[0], sb[0]};
+#pragma unroll
+    for (int k = 1; k < CPT; ++k) {
+      off[0] = __dadd_rn(off[0], sa[k]);
+      off[1] = __dadd_rn(off[1], sb[k]);
+    }
+    thread_offsets<2>(off, wt[buf]);
+    {
+      double ra = off[0], rb = off[1];
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        ra = __dadd_rn(ra, sa[k]);
+        rb = __dadd_rn(rb, sb[k]);
+        pre[buf][0][threadIdx.x * CPT + k + 1] = ra;
+        pre[buf][1][threadIdx.x * CPT + k + 1] = rb;
+      }
+    }
     __syncthreads();
-    if (active) {
-      const double ma = div_rb(__dsub_rn(pre[buf][0][hi], pre[buf][0][lo]), kk, rkk);
-      const double mb = div_rb(__dsub_rn(pre[buf][1][hi], pre[buf][1][lo]), kk, rkk);
-      const uint8_t* px = frame + ((int64_t)y * W + xo) * 3;
-      const uint32_t R = px[0], G = px[1], B = px[2];
-      const double g = guide_t(T, R, G, B);
-      double t = fmin(fmax(__dadd_rn(__dmul_rn(ma, g), mb), 0.0), 1.0);
-      t = fmax(t, t_min);  // pipeline.py:203
-      const double rt = __drcp_rn(t);
-      const double x0v = recover_x(T.t[R], A0, t, rt), x1v = recover_x(T.t[G], A1, t, rt),
-                   x2v = recover_x(T.t[B], A2, t, rt);
-      if (MODE == 0) {
-        uint8_t* o = out + (int64_t)f * out_fs + ((int64_t)y * W + xo) * 3;
-        o[0] = (uint8_t)quantize_thr(x0v, s_thr);
-        o[1] = (uint8_t)quantize_thr(x1v, s_thr);
-        o[2] = (uint8_t)quantize_thr(x2v, s_thr);
-      } else {
-        t_out[fo + (int64_t)y * W + xo] = t;
-        if (gamma_is_one) {
-          acc0 = __dadd_rn(acc0, x0v);
-          acc1 = __dadd_rn(acc1, x1v);
-          acc2 = __dadd_rn(acc2, x2v);
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      const int j = k * kThreads + (int)threadIdx.x;
+      if (j < sw && x0 + j < W) {
+        const int hi = j + 2 * r + 1;
+        const double ma = div_rb(__dsub_rn(pre[buf][0][hi], pre[buf][0][j]), kk, rkk);
+        const double mb = div_rb(__dsub_rn(pre[buf][1][hi], pre[buf][1][j]), kk, rkk);
+        const int64_t pix = (int64_t)y * W + x0 + j;
+        const uint8_t* px = frame + pix * 3;
+        const uint32_t R = px[0], G = px[1], B = px[2];
+        const double g = guide_t(T, R, G, B);
+        double t = fmin(fmax(__dadd_rn(__dmul_rn(ma, g), mb), 0.0), 1.0);
+        t = fmax(t, t_min);  // pipeline.py:203
+        const double rt = __drcp_rn(t);
+        const double x0v = recover_x(T.t[R], A0, t, rt), x1v = recover_x(T.t[G], A1, t, rt),
+                     x2v = recover_x(T.t[B], A2, t, rt);
+        if (MODE == 0) {
+          uint8_t* o = out + (int64_t)f * out_fs + pix * 3;
+          o[0] = (uint8_t)quantize_thr(x0v, s_thr);
+          o[1] = (uint8_t)quantize_thr(x1v, s_thr);
+          o[2] = (uint8_t)quantize_thr(x2v, s_thr);
         } else {
-          acc0 = __dadd_rn(acc0, fmin(fmax(pow(x0v, inv_gamma), 0.0), 1.0));
-          acc1 = __dadd_rn(acc1, fmin(fmax(pow(x1v, inv_gamma), 0.0), 1.0));
-          acc2 = __dadd_rn(acc2, fmin(fmax(pow(x2v, inv_gamma), 0.0), 1.0));
+          t_out[fo + pix] = t;
+          if (gamma_is_one) {
+            acc0 = __dadd_rn(acc0, x0v);
+            acc1 = __dadd_rn(acc1, x1v);
+            acc2 = __dadd_rn(acc2, x2v);
+          } else {
+            acc0 = __dadd_rn(acc0, pow_unit(x0v, inv_gamma));
+            acc1 = __dadd_rn(acc1, pow_unit(x1v, inv_gamma));
+            acc2 = __dadd_rn(acc2, pow_unit(x2v, inv_gamma));
+          }
         }
       }
     }
@@ -280,35 +365,78 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
       for (int c = 0; c < 3; ++c) red[c * 8 + (threadIdx.x >> 5)] = v3[c];
     __syncthreads();
     if (threadIdx.x < 3) {
-      double s = 0.0;
-      for (int w = 0; w < kCols / 32; ++w) s = __dadd_rn(s, red[threadIdx.x * 8 + w]);
+      double sum = 0.0;
+      for (int w = 0; w < kThreads / 32; ++w) sum = __dadd_rn(sum, red[threadIdx.x * 8 + w]);
       const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-      part[((int64_t)f * gridDim.x * gridDim.y + cta) * 3 + threadIdx.x] = s;
+      part[((int64_t)f * gridDim.x * gridDim.y + cta) * 3 + threadIdx.x] = sum;
     }
   }
 }
 
-// gray-world apply: gains from the per-CTA partial sums, then out = u8(clip(g * gain)).
+// ------------------------------------------------------- gray-world balance ----
+// Per frame and channel: gains from the per-CTA sums (recover.py:57-69), then
+// thr[k] = smallest recovered value x in [0, 1] whose output byte
+// u8(clip(clip(x^(1/gamma)) * gain)) is >= k (bisection on the bit patterns of
+// non-negative doubles, which order like the values), +inf where unreachable.
+// The byte of a sample is then the number of thresholds <= x.
+__device__ __forceinline__ int balanced_byte(double x, double inv_gamma, int gamma_is_one, double gain, int copy) {
+  const double g = gamma_is_one ? x : fmin(fmax(pow(x, inv_gamma), 0.0), 1.0);
+  return quantize_unit(copy ? g : fmin(fmax(__dmul_rn(g, gain), 0.0), 1.0));
+}
+
 __global__ void __launch_bounds__(256)
-k_gf_apply(const uint8_t* __restrict__ in, int64_t in_fs, int64_t npx, const double* __restrict__ t_in,
-           const double* __restrict__ airlight, double inv_gamma, int gamma_is_one, const double* __restrict__ part,
-           int nparts, uint8_t* __restrict__ out, int64_t out_fs) {
-  __shared__ double s_gain[3], s_f[256];
+k_gf_thresholds(const double* __restrict__ part, int nparts, int64_t npx, double inv_gamma, int gamma_is_one,
+                double* __restrict__ thr_out /* [n][3][256] */) {
+  __shared__ double s_gain;
   __shared__ int s_copy;
-  const int f = blockIdx.y;
-  s_f[threadIdx.x] = u8f(threadIdx.x);
+  const int f = blockIdx.y, c = blockIdx.x;
   if (threadIdx.x == 0) {
     double m[3];
-    for (int c = 0; c < 3; ++c) {
-      double s = 0.0;
-      for (int b = 0; b < nparts; ++b) s = __dadd_rn(s, part[((int64_t)f * nparts + b) * 3 + c]);
-      m[c] = __ddiv_rn(s, (double)npx);
+    for (int ch = 0; ch < 3; ++ch) {
+      double sum = 0.0;
+      for (int b = 0; b < nparts; ++b) sum = __dadd_rn(sum, part[((int64_t)f * nparts + b) * 3 + ch]);
+      m[ch] = __ddiv_rn(sum, (double)npx);
     }
     const bool degenerate = fmin(fmin(m[0], m[1]), m[2]) < 1e-6;
     const double mm = __ddiv_rn(__dadd_rn(__dadd_rn(m[0], m[1]), m[2]), 3.0);
-    for (int c = 0; c < 3; ++c) s_gain[c] = degenerate ? 1.0 : fmin(fmax(__ddiv_rn(mm, m[c]), 0.5), 2.0);
+    s_gain = degenerate ? 1.0 : fmin(fmax(__ddiv_rn(mm, m[c]), 0.5), 2.0);
     s_copy = degenerate;
   }
+  __syncthreads();
+  const int k = threadIdx.x;
+  double* out = thr_out + ((int64_t)f * 3 + c) * 256;
+  if (k == 0) {
+    out[0] = -1.0;
+    return;
+  }
+  const double gain = s_gain;
+  const int copy = s_copy;
+  if (balanced_byte(1.0, inv_gamma, gamma_is_one, gain, copy) < k) {
+    out[k] = __longlong_as_double(0x7ff0000000000000LL);  // +inf: level never reached
+    return;
+  }
+  if (balanced_byte(0.0, inv_gamma, gamma_is_one, gain, copy) >= k) {
+    out[k] = 0.0;
+    return;
+  }
+  long long lo = 0, hi = __double_as_longlong(1.0);  // byte(lo) < k <= byte(hi)
+  while (hi - lo > 1) {
+    const long long mid = lo + (hi - lo) / 2;
+    if (balanced_byte(__longlong_as_double(mid), inv_gamma, gamma_is_one, gain, copy) >= k) hi = mid;
+    else lo = mid;
+  }
+  out[k] = __longlong_as_double(hi);
+}
+
+// gray-world apply: out = #thresholds <= recovered x (per channel).
+__global__ void __launch_bounds__(256)
+k_gf_apply(const uint8_t* __restrict__ in, int64_t in_fs, int64_t npx, const double* __restrict__ t_in,
+           const double* __restrict__ airlight, const double* __restrict__ thr, uint8_t* __restrict__ out,
+           int64_t out_fs) {
+  __shared__ double s_f[256], s_thr[3][256];
+  const int f = blockIdx.y;
+  s_f[threadIdx.x] = u8f(threadIdx.x);
+  for (int c = 0; c < 3; ++c) s_thr[c][threadIdx.x] = thr[((int64_t)f * 3 + c) * 256 + threadIdx.x];
   __syncthreads();
   const double A0 = airlight[3 * f], A1 = airlight[3 * f + 1], A2 = airlight[3 * f + 2];
   const uint8_t* fi = in + (int64_t)f * in_fs;
@@ -316,23 +444,28 @@ k_gf_apply(const uint8_t* __restrict__ in, int64_t in_fs, int64_t npx, const dou
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npx; p += (int64_t)gridDim.x * blockDim.x) {
     const double t = t_in[(int64_t)f * npx + p];
     const double rt = __drcp_rn(t);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const double x = recover_x(s_f[fi[3 * p + c]], c == 0 ? A0 : (c == 1 ? A1 : A2), t, rt);
-      const double g = gamma_is_one ? x : fmin(fmax(pow(x, inv_gamma), 0.0), 1.0);
-      fo[3 * p + c] = (uint8_t)quantize_unit(s_copy ? g : fmin(fmax(__dmul_rn(g, s_gain[c]), 0.0), 1.0));
-    }
+    fo[3 * p + 0] = (uint8_t)quantize_thr(recover_x(s_f[fi[3 * p + 0]], A0, t, rt), s_thr[0]);
+    fo[3 * p + 1] = (uint8_t)quantize_thr(recover_x(s_f[fi[3 * p + 1]], A1, t, rt), s_thr[1]);
+    fo[3 * p + 2] = (uint8_t)quantize_thr(recover_x(s_f[fi[3 * p + 2]], A2, t, rt), s_thr[2]);
   }
+}
+
+// Columns per thread: 2 (512-column strips) unless that leaves too few CTAs.
+int guided_cpt(int H, int W, int r, int n) {
+  if (2 * r >= kThreads) return 2;  // only the wide strip fits the window
+  const int sw2 = 2 * kThreads - 2 * r;
+  const int64_t ctas2 = (int64_t)((W + sw2 - 1) / sw2) * n * ((H + 15) / 16);
+  return ctas2 >= 2 * 148 ? 2 : 1;
 }
 
 }  // namespace
 
 // Rows per CTA segment: long segments amortise the 2r+1-row warm-up of the
-// sliding sums, short ones give small batches enough CTAs (>= ~4 per SM).
-int guided_seg_rows(int H, int W, int r, int n) {
-  const int sw = kCols - 2 * r;
+// sliding sums, short ones give small batches enough CTAs.
+int guided_seg_rows(int H, int W, int r, int n, int cpt) {
+  const int sw = kThreads * cpt - 2 * r;
   const int64_t strips = (int64_t)((W + sw - 1) / sw) * n;
-  const int64_t want = 8 * 148;  // ~2 waves at 4 resident CTAs per SM
+  const int64_t want = 6 * 148;
   int64_t segs = std::max<int64_t>(1, (want + strips - 1) / strips);
   int seg = (int)((H + segs - 1) / segs);
   seg = std::max(seg, std::min(H, std::max(16, r)));  // the 2r+1-row warm-up is cheap next to a row
@@ -348,44 +481,56 @@ int guided_chunk(int n, int H, int W, bool balance) {
 size_t guided_ws_bytes(int n, int H, int W, int r, bool balance) {
   const int64_t npx = (int64_t)H * W;
   const int c = guided_chunk(n, H, W, balance);
-  const int sw = kCols - 2 * r;
-  const int seg = guided_seg_rows(H, W, r, c);
-  const int64_t parts = (int64_t)((W + sw - 1) / sw) * ((H + seg - 1) / seg);
-  size_t b = 16ull * npx * c;                             // a, b
-  if (balance) b += 8ull * npx * c + 24ull * parts * c;   // t~, partial sums
+  size_t b = 16ull * npx * c;                                            // a, b
+  if (balance) {
+    int64_t parts = 0;
+    for (int cpt = 1; cpt <= 2; ++cpt) {  // either strip width may be chosen for the chunk
+      const int sw = kThreads * cpt - 2 * r;
+      if (sw < 1) continue;
+      const int seg = guided_seg_rows(H, W, r, c, cpt);
+      parts = std::max<int64_t>(parts, (int64_t)((W + sw - 1) / sw) * ((H + seg - 1) / seg));
+    }
+    b += 8ull * npx * c + 24ull * parts * c + 3 * 256 * 8ull * c;       // t~, partial sums, thresholds
+  }
   return b;
 }
 
 cudaError_t guided_recover_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, int r, double eps,
                               const double* airlight, double omega, double t_min, const double* thr, double gamma,
                               bool balance, uint8_t* out, int64_t out_fs, void* ws, cudaStream_t st) {
-  if (r < 1 || 2 * r >= kCols) return cudaErrorInvalidValue;
+  if (r < 1 || r > kGuidedMaxRadius) return cudaErrorInvalidValue;
   const int64_t npx = (int64_t)H * W;
-  const int sw = kCols - 2 * r;
   const int chunk = guided_chunk(n, H, W, balance);
   const double inv_g = 1.0 / gamma;
   const int g1 = gamma == 1.0 ? 1 : 0;
   for (int f0 = 0; f0 < n; f0 += chunk) {
     const int c = std::min(chunk, n - f0);
-    const int seg = guided_seg_rows(H, W, r, c);
+    const int cpt = guided_cpt(H, W, r, c);
+    const int sw = kThreads * cpt - 2 * r;
+    const int seg = guided_seg_rows(H, W, r, c, cpt);
     dim3 grid((W + sw - 1) / sw, (H + seg - 1) / seg, c);
     const uint8_t* fin = in + (int64_t)f0 * in_fs;
     uint8_t* fout = out + (int64_t)f0 * out_fs;
     const double* fA = airlight + 3 * f0;
     double* a = static_cast<double*>(ws);
     double* b = a + npx * c;
-    k_gf_pass1<<<grid, kCols, 0, st>>>(fin, in_fs, H, W, r, seg, eps, fA, omega, t_min, a, b);
+    double* t = b + npx * c;
+    double* part = t + npx * c;
+    if (cpt == 2) k_gf_pass1<2><<<grid, kThreads, 0, st>>>(fin, in_fs, H, W, r, seg, eps, fA, omega, t_min, a, b);
+    else k_gf_pass1<1><<<grid, kThreads, 0, st>>>(fin, in_fs, H, W, r, seg, eps, fA, omega, t_min, a, b);
     if (!balance) {
-      k_gf_pass2<0><<<grid, kCols, 0, st>>>(fin, in_fs, H, W, r, seg, a, b, fA, t_min, thr, inv_g, g1, fout, out_fs,
-                                            nullptr, nullptr);
+      auto k2 = cpt == 2 ? k_gf_pass2<0, 2> : k_gf_pass2<0, 1>;
+      k2<<<grid, kThreads, 0, st>>>(fin, in_fs, H, W, r, seg, a, b, fA, t_min, thr, inv_g, g1, fout, out_fs,
+                                    nullptr, nullptr);
     } else {
-      double* t = b + npx * c;
-      double* part = t + npx * c;
-      k_gf_pass2<1><<<grid, kCols, 0, st>>>(fin, in_fs, H, W, r, seg, a, b, fA, t_min, thr, inv_g, g1, fout, out_fs,
-                                            t, part);
+      auto k2 = cpt == 2 ? k_gf_pass2<1, 2> : k_gf_pass2<1, 1>;
+      k2<<<grid, kThreads, 0, st>>>(fin, in_fs, H, W, r, seg, a, b, fA, t_min, thr, inv_g, g1, fout, out_fs, t,
+                                    part);
       const int nparts = grid.x * grid.y;
-      dim3 g2((unsigned)std::min<int64_t>(4096, (npx + 255) / 256), c);
-      k_gf_apply<<<g2, 256, 0, st>>>(fin, in_fs, npx, t, fA, inv_g, g1, part, nparts, fout, out_fs);
+      double* bthr = part + 3LL * nparts * c;
+      k_gf_thresholds<<<dim3(3, c), 256, 0, st>>>(part, nparts, npx, inv_g, g1, bthr);
+      dim3 g2((unsigned)std::min<int64_t>(2048, (npx + 255) / 256), c);
+      k_gf_apply<<<g2, 256, 0, st>>>(fin, in_fs, npx, t, fA, bthr, fout, out_fs);
     }
   }
   return cudaGetLastError();

@@ -183,7 +183,7 @@ def _needs_resize(params, h, w):
     return (int(rw), int(rh)) != (w, h)
 
 
-GUIDED_MAX_RADIUS = 127  # dhz::kGuidedMaxRadius (fused guided filter: 2r < 256 columns per strip)
+GUIDED_MAX_RADIUS = 255  # dhz::kGuidedMaxRadius (fused guided filter: 2r < 512 columns per strip)
 
 
 def _native_ok(params, h, w, want_maps=False):

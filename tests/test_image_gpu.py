@@ -49,7 +49,7 @@ def test_synthetic_image(oracle, balance):
     _check(frames, _params(white_balance=balance), oracle)
 
 
-@pytest.mark.parametrize("r", [1, 2, 5, 40, 100, 127])
+@pytest.mark.parametrize("r", [1, 2, 5, 40, 100, 127, 128, 255])
 def test_guided_radii(oracle, r):
     from paper_2512_16609_b200.synthetic import make_frames
 
@@ -87,6 +87,15 @@ def test_many_frames_one_call(oracle):
 def test_wide_radius_uses_float_path():
     from paper_2512_16609_b200.pipeline import _native_ok
 
-    assert not _native_ok(_params(guided_radius=128), 64, 64)
+    assert not _native_ok(_params(guided_radius=256), 64, 64)
     assert not _native_ok(_params(), 64, 64, want_maps=True)
     assert _native_ok(_params(), 64, 64)
+
+
+@pytest.mark.parametrize("balance", [False, True])
+def test_wide_strips_batch(oracle, balance):
+    # enough CTAs for the two-columns-per-thread (512-column) strips
+    from paper_2512_16609_b200.synthetic import make_frames
+
+    frames = make_frames("c2", frames=8, width=600, height=640).numpy()
+    _check(frames, _params(guided_radius=30, white_balance=balance), oracle)

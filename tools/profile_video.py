@@ -1,4 +1,4 @@
-"""Small driver for ncu: runs the fused video pipeline a few times on a 1080p batch."""
+"""Small driver for ncu: runs the fused pipeline (video, or image mode with --image R) a few times."""
 import argparse
 import os
 import sys
@@ -18,11 +18,13 @@ ap.add_argument("--height", type=int, default=1080)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--balance", action="store_true")
 ap.add_argument("--radius", type=int, default=7)
+ap.add_argument("--image", type=int, default=0, help="guided radius; > 0 selects image mode")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 scene = Scene(a.width, a.height, 3000, dev)
 frames = torch.stack([scene.hazy_u8(f, 3000 + f, 0.6, (0.85, 0.87, 0.9)) for f in range(a.frames)])
-params = DehazeParams(resize_to=None, white_balance=a.balance, patch_radius=a.radius)
+params = DehazeParams(resize_to=None, white_balance=a.balance, patch_radius=a.radius,
+                      mode="image" if a.image > 0 else "video", guided_radius=max(a.image, 1))
 eng = engine_for(dev)
 for _ in range(a.iters):
     out, air = eng.run(frames, params)
