@@ -190,6 +190,21 @@ __device__ __forceinline__ int quantize_thr(double x, const double* __restrict__
   return lo;
 }
 
+// Same result as quantize_thr for ANY start level k (walks up/down the monotone
+// thresholds); a good guess makes it 1-2 shared loads instead of 8.
+__device__ __forceinline__ int quantize_thr_from(double x, const double* __restrict__ thr, int k) {
+  while (k < 255 && thr[k + 1] <= x) ++k;
+  while (k > 0 && thr[k] > x) --k;
+  return k;
+}
+
+// fp32 estimate of the output byte u8(clip(x^(1/gamma) * gain)): only a start
+// level for quantize_thr_from, never the answer itself.
+__device__ __forceinline__ int guess_byte(double x, float inv_gamma, float gain) {
+  const float g = __powf((float)x, inv_gamma) * gain;
+  return __float2int_rn(fminf(fmaxf(g, 0.0f), 1.0f) * 255.0f);
+}
+
 // floor(clip(y)*255 + 0.5) with the reference's separate roundings (imageops.py:32-36).
 __device__ __forceinline__ int quantize_unit(double y) {
   y = fmin(fmax(y, 0.0), 1.0);

@@ -49,12 +49,13 @@ __device__ __forceinline__ double div_rb(double a, double b, double rb) {
 // gray-world channel sums, where per-sample errors of ~1e-16 are far below the
 // reference's own summation rounding.  Bytes are never derived from it.
 __device__ __forceinline__ double pow_unit(double x, double e) {
-  if (!(x > 0.0)) return 0.0;
+  if (!(x >= 0x1p-1000)) return 0.0;  // (recovered values are 0 or far above this)
   if (x >= 1.0) return 1.0;
-  int ex;
-  double m = frexp(x, &ex);                 // x = m * 2^ex, m in [0.5, 1)
+  const long long bits = __double_as_longlong(x);
+  int ex = (int)(bits >> 52) - 1022;                                           // x = m * 2^ex
+  double m = __longlong_as_double((bits & 0x000fffffffffffffLL) | 0x3fe0000000000000LL);  // m in [0.5, 1)
   if (m < 0.70710678118654752) { m = m * 2.0; ex -= 1; }   // m in [sqrt(1/2), sqrt(2))
-  const double s = __ddiv_rn(m - 1.0, m + 1.0);
+  const double s = (m - 1.0) * __drcp_rn(m + 1.0);
   const double s2 = s * s;
   double p = 1.0 / 23;
   p = fma(p, s2, 1.0 / 21); p = fma(p, s2, 1.0 / 19); p = fma(p, s2, 1.0 / 17); p = fma(p, s2, 1.0 / 15);
@@ -63,7 +64,7 @@ __device__ __forceinline__ double pow_unit(double x, double e) {
   const double lnm = 2.0 * fma(p * s2, s, s);  // 2 atanh(s) = ln(m)
   constexpr double kLn2Hi = 6.93147180369123816490e-01, kLn2Lo = 1.90821492927058770002e-10;
   const double y = e * fma((double)ex, kLn2Hi, fma((double)ex, kLn2Lo, lnm));   // e * ln(x) <= 0
-  if (y < -700.0) return 0.0;
+  if (y < -700.0) return 0.0;  // keeps 2^k normal below
   const double k = rint(y * 1.44269504088896340736);
   const double r = fma(-k, kLn2Lo, fma(-k, kLn2Hi, y));  // |r| <= ~0.35
   double q = 1.0 / 6227020800.0;                          // 1/13!
@@ -72,7 +73,7 @@ __device__ __forceinline__ double pow_unit(double x, double e) {
   q = fma(q, r, 1.0 / 720.0);       q = fma(q, r, 1.0 / 120.0);      q = fma(q, r, 1.0 / 24.0);
   q = fma(q, r, 1.0 / 6.0);         q = fma(q, r, 0.5);              q = fma(q, r, 1.0);
   q = fma(q, r, 1.0);
-  return ldexp(q, (int)k);
+  return q * __longlong_as_double((long long)((int)k + 1023) << 52);  // k in [-1010, 0]
 }
 
 // Per-CTA tables: exact u8 -> fp64 products used by the guide and the coarse t.
@@ -89,6 +90,16 @@ __device__ __forceinline__ void load_guide(GuideTables& T, int v, double x) {
 
 __device__ __forceinline__ double guide_t(const GuideTables& T, uint32_t r, uint32_t g, uint32_t b) {
   return fmin(fmax(__dadd_rn(__dadd_rn(T.wr[r], T.wg[g]), T.wb[b]), 0.0), 1.0);
+}
+
+// The same guide value without table lookups (shared-memory traffic binds pass 1):
+// RN(v/255) as div_rb(v, 255, RN(1/255)), then the three weighted products.
+__device__ __forceinline__ double guide_arith(uint32_t r, uint32_t g, uint32_t b) {
+  constexpr double k255 = 255.0;
+  constexpr double rk = 0x1.0101010101010p-8;  // RN(1/255)
+  const double xr = div_rb((double)r, k255, rk), xg = div_rb((double)g, k255, rk), xb = div_rb((double)b, k255, rk);
+  const double v = __dadd_rn(__dadd_rn(__dmul_rn(0.299, xr), __dmul_rn(0.587, xg)), __dmul_rn(0.114, xb));
+  return fmin(fmax(v, 0.0), 1.0);
 }
 
 // tot[q] (this thread's sum over its columns) -> the CTA-exclusive prefix before
@@ -117,11 +128,17 @@ __device__ __forceinline__ void thread_offsets(double (&tot)[NQ], double (*wt)[k
     tot[q] = lane == 0 ? 0.0 : ex;
   }
   __syncthreads();
+  // carries: every warp scans the 8 warp totals with shuffles (lanes 0..7)
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
-    double base = 0.0;
-    for (int w = 0; w < wid; ++w) base = __dadd_rn(base, wt[q][w]);
-    tot[q] = __dadd_rn(base, tot[q]);
+    double c = (lane < kThreads / 32) ? wt[q][lane] : 0.0;
+#pragma unroll
+    for (int o = 1; o < kThreads / 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, c, o);
+      if (lane >= o) c = __dadd_rn(c, y);
+    }
+    const double base = __shfl_sync(0xffffffffu, c, (wid + 31) & 31);  // inclusive total of warps < wid
+    tot[q] = wid == 0 ? tot[q] : __dadd_rn(base, tot[q]);
   }
 }
 
@@ -159,7 +176,7 @@ k_gf_pass1(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
   auto feat = [&](int y, int k, double& g, double& p) {
     const uint8_t* px = frame + (int64_t)min(max(y, 0), H - 1) * pitch + xc[k];
     const uint32_t R = px[0], G = px[1], B = px[2];
-    g = guide_t(T, R, G, B);
+    g = guide_arith(R, G, B);
     p = T.t[min(min(R, G), B)];
   };
   // vertical window sums for output row y0: rows y0-r .. y0+r (clamped)
@@ -335,9 +352,10 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
                      x2v = recover_x(T.t[B], A2, t, rt);
         if (MODE == 0) {
           uint8_t* o = out + (int64_t)f * out_fs + pix * 3;
-          o[0] = (uint8_t)quantize_thr(x0v, s_thr);
-          o[1] = (uint8_t)quantize_thr(x1v, s_thr);
-          o[2] = (uint8_t)quantize_thr(x2v, s_thr);
+          const float ig = (float)inv_gamma;
+          o[0] = (uint8_t)quantize_thr_from(x0v, s_thr, guess_byte(x0v, ig, 1.0f));
+          o[1] = (uint8_t)quantize_thr_from(x1v, s_thr, guess_byte(x1v, ig, 1.0f));
+          o[2] = (uint8_t)quantize_thr_from(x2v, s_thr, guess_byte(x2v, ig, 1.0f));
         } else {
           t_out[fo + pix] = t;
           if (gamma_is_one) {
@@ -386,7 +404,7 @@ __device__ __forceinline__ int balanced_byte(double x, double inv_gamma, int gam
 
 __global__ void __launch_bounds__(256)
 k_gf_thresholds(const double* __restrict__ part, int nparts, int64_t npx, double inv_gamma, int gamma_is_one,
-                double* __restrict__ thr_out /* [n][3][256] */) {
+                double* __restrict__ thr_out /* [n][3][256] */, float* __restrict__ gains_out /* [n][3] */) {
   __shared__ double s_gain;
   __shared__ int s_copy;
   const int f = blockIdx.y, c = blockIdx.x;
@@ -405,6 +423,7 @@ k_gf_thresholds(const double* __restrict__ part, int nparts, int64_t npx, double
   __syncthreads();
   const int k = threadIdx.x;
   double* out = thr_out + ((int64_t)f * 3 + c) * 256;
+  if (k == 0) gains_out[3 * f + c] = (float)s_gain;
   if (k == 0) {
     out[0] = -1.0;
     return;
@@ -428,25 +447,50 @@ k_gf_thresholds(const double* __restrict__ part, int nparts, int64_t npx, double
   out[k] = __longlong_as_double(hi);
 }
 
-// gray-world apply: out = #thresholds <= recovered x (per channel).
+// gray-world apply: out = #thresholds <= recovered x (per channel).  Four
+// independent pixels per thread and iteration keep enough loads in flight.
 __global__ void __launch_bounds__(256)
 k_gf_apply(const uint8_t* __restrict__ in, int64_t in_fs, int64_t npx, const double* __restrict__ t_in,
-           const double* __restrict__ airlight, const double* __restrict__ thr, uint8_t* __restrict__ out,
-           int64_t out_fs) {
+           const double* __restrict__ airlight, const double* __restrict__ thr, const float* __restrict__ gains,
+           double inv_gamma, uint8_t* __restrict__ out, int64_t out_fs) {
+  constexpr int U = 4;
   __shared__ double s_f[256], s_thr[3][256];
   const int f = blockIdx.y;
   s_f[threadIdx.x] = u8f(threadIdx.x);
   for (int c = 0; c < 3; ++c) s_thr[c][threadIdx.x] = thr[((int64_t)f * 3 + c) * 256 + threadIdx.x];
   __syncthreads();
   const double A0 = airlight[3 * f], A1 = airlight[3 * f + 1], A2 = airlight[3 * f + 2];
+  const float gn0 = gains[3 * f], gn1 = gains[3 * f + 1], gn2 = gains[3 * f + 2];
+  const float ig = (float)inv_gamma;
   const uint8_t* fi = in + (int64_t)f * in_fs;
   uint8_t* fo = out + (int64_t)f * out_fs;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npx; p += (int64_t)gridDim.x * blockDim.x) {
-    const double t = t_in[(int64_t)f * npx + p];
-    const double rt = __drcp_rn(t);
-    fo[3 * p + 0] = (uint8_t)quantize_thr(recover_x(s_f[fi[3 * p + 0]], A0, t, rt), s_thr[0]);
-    fo[3 * p + 1] = (uint8_t)quantize_thr(recover_x(s_f[fi[3 * p + 1]], A1, t, rt), s_thr[1]);
-    fo[3 * p + 2] = (uint8_t)quantize_thr(recover_x(s_f[fi[3 * p + 2]], A2, t, rt), s_thr[2]);
+  const double* ft = t_in + (int64_t)f * npx;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < npx; p0 += U * stride) {
+    double t[U];
+    uint32_t v[U][3];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = min(p0 + u * stride, npx - 1);
+      t[u] = ft[p];
+      v[u][0] = fi[3 * p];
+      v[u][1] = fi[3 * p + 1];
+      v[u][2] = fi[3 * p + 2];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = p0 + u * stride;
+      if (p < npx) {
+        const double rt = __drcp_rn(t[u]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double Ac = c == 0 ? A0 : (c == 1 ? A1 : A2);
+          const float gc = c == 0 ? gn0 : (c == 1 ? gn1 : gn2);
+          const double x = recover_x(s_f[v[u][c]], Ac, t[u], rt);
+          fo[3 * p + c] = (uint8_t)quantize_thr_from(x, s_thr[c], guess_byte(x, ig, gc));
+        }
+      }
+    }
   }
 }
 
@@ -490,7 +534,7 @@ size_t guided_ws_bytes(int n, int H, int W, int r, bool balance) {
       const int seg = guided_seg_rows(H, W, r, c, cpt);
       parts = std::max<int64_t>(parts, (int64_t)((W + sw - 1) / sw) * ((H + seg - 1) / seg));
     }
-    b += 8ull * npx * c + 24ull * parts * c + 3 * 256 * 8ull * c;       // t~, partial sums, thresholds
+    b += 8ull * npx * c + 24ull * parts * c + 3 * 256 * 8ull * c + 16ull * c;  // t~, sums, thresholds, gains
   }
   return b;
 }
@@ -528,9 +572,10 @@ cudaError_t guided_recover_u8(const uint8_t* in, int64_t in_fs, int n, int H, in
                                     part);
       const int nparts = grid.x * grid.y;
       double* bthr = part + 3LL * nparts * c;
-      k_gf_thresholds<<<dim3(3, c), 256, 0, st>>>(part, nparts, npx, inv_g, g1, bthr);
-      dim3 g2((unsigned)std::min<int64_t>(2048, (npx + 255) / 256), c);
-      k_gf_apply<<<g2, 256, 0, st>>>(fin, in_fs, npx, t, fA, bthr, fout, out_fs);
+      float* gains = reinterpret_cast<float*>(bthr + 3LL * 256 * c);
+      k_gf_thresholds<<<dim3(3, c), 256, 0, st>>>(part, nparts, npx, inv_g, g1, bthr, gains);
+      dim3 g2((unsigned)std::max<int64_t>(1, std::min<int64_t>(2048, (npx + 1023) / 1024)), c);
+      k_gf_apply<<<g2, 256, 0, st>>>(fin, in_fs, npx, t, fA, bthr, gains, inv_g, fout, out_fs);
     }
   }
   return cudaGetLastError();
