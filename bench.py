@@ -41,11 +41,34 @@ CONFIG_PARAMS = {
     "c4": dict(resize_to=None, white_balance=True),
     "c2": dict(mode="image", resize_to=None, guided_radius=30, guided_eps=1e-3),
     "c5": dict(mode="image", resize_to=None, patch_radius=15, guided_radius=60, guided_eps=1e-3),
+    # the reference's default DehazeParams() (resize_to=(640, 480)) on the C3 frames (SURVEY §8(d),
+    # "secondary row"; throughput counted in input megapixels)
+    "c3d": dict(),
 }
+
+
+def engine_for_sizes(params, H, W):
+    from paper_2512_16609_b200.engine import FrameEngine
+
+    return FrameEngine.working_size(params, H, W)
+
+
+def _size_note(params):
+    if params.resize_to is None:
+        return "native resolution"
+    return f"resized to {params.resize_to[0]}x{params.resize_to[1]} (reference default; MP/s counts input pixels)"
+
+
+def _base(cfg):
+    """Synthetic frame config behind a bench config ("c3d" runs on the C3 frames)."""
+    return cfg[:2]
 # algorithmic HBM bytes per pixel (SURVEY.md §8(d)): dark 4 + select 1 + recover 6 (+3 balance);
 # image mode: dark 4 + select 1 + guided pass 1 (read I 3, write a,b 16) + pass 2 (read a,b 16,
 # read I 3, write O 3) = 46, + balance (pass 2 writes t~ 8, apply reads I 3 + t~ 8, writes O 3) = 62
-ALG_BYTES = {"c1": 11, "c3": 11, "c4": 14, "c2": 62, "c5": 62}
+ALG_BYTES = {"c1": 11, "c3": 11, "c4": 14, "c2": 62, "c5": 62,
+             # resize path per INPUT pixel (1080p -> 640x480, 0.148 output px per input px): dark pass
+             # reads I 3 + writes dark 8*0.148, select reads dark 8*0.148, recover reads I 3 + writes 3*0.148
+             "c3d": round(6 + 19 * (640 * 480) / (1920 * 1080), 2)}
 GUIDED_BYTES = {False: 41, True: 57}
 
 
@@ -156,11 +179,11 @@ def run_reference(args):
     from paper_2512_16609_b200.synthetic import CONFIGS, make_frames
 
     cfg = args.config
-    spec = CONFIGS[cfg]
+    spec = CONFIGS[_base(cfg)]
     params = DehazeParams(**CONFIG_PARAMS[cfg])
     workers = os.cpu_count() or 1
     sample = max(1, min(spec["frames"], workers))
-    frames = make_frames(cfg, frames=sample).numpy()
+    frames = make_frames(_base(cfg), frames=sample).numpy()
     npx = frames.shape[1] * frames.shape[2]
     from oracle.dehaze_oracle import process_stream
 
@@ -188,7 +211,7 @@ def run_reference(args):
         "dtype": "f64",
         "data": "synthetic (seeded BASELINE generator)",
         "config": {"workload": f"{cfg}: {sample} of {spec['frames']} frames {spec['width']}x{spec['height']} "
-                               f"per step, {params.mode} mode, native resolution",
+                               f"per step, {params.mode} mode, " + _size_note(params),
                    "frames_per_step": sample},
         "cpu_baseline": {"value": round(value, 3), "unit": "MP/s", "cores": workers, "kind": "port",
                          "sample": f"{sample} frames per step, oracle/dehaze_oracle.py process_stream "
@@ -228,28 +251,30 @@ def main():
     from paper_2512_16609_b200.synthetic import CONFIGS, Scene, make_frames
 
     cfg = args.config
-    spec = CONFIGS[cfg]
+    spec = CONFIGS[_base(cfg)]
     params = DehazeParams(**CONFIG_PARAMS[cfg])
     n, H, W = spec["frames"], spec["height"], spec["width"]
     npx = H * W
+    OH, OW = engine_for_sizes(params, H, W)
 
     # ---- inputs: this rank's shard, generated on the device -------------------
     frames = torch.empty((n, H, W, 3), dtype=torch.uint8, device=dev)
-    if cfg in ("c3", "c4", "c1", "c2"):
-        scene = Scene(W, H, 1000 * int(cfg[1:]), dev)
+    base = _base(cfg)
+    if base in ("c3", "c4", "c1", "c2"):
+        scene = Scene(W, H, 1000 * int(base[1:]), dev)
         for f in range(n):
             g = rank * n + f
-            beta = 0.65 - 0.15 * math.cos(2 * math.pi * g / 300.0) if cfg in ("c3", "c4") else 0.6
-            frames[f] = scene.hazy_u8(g, 1000 * int(cfg[1:]) + g, beta, spec["airlight"])
+            beta = 0.65 - 0.15 * math.cos(2 * math.pi * g / 300.0) if base in ("c3", "c4") else 0.6
+            frames[f] = scene.hazy_u8(g, 1000 * int(base[1:]) + g, beta, spec["airlight"])
     else:
-        make_frames(cfg, frames=n, device=dev, out=frames)
+        make_frames(base, frames=n, device=dev, out=frames)
     torch.cuda.synchronize()
 
     from paper_2512_16609_b200.pipeline import _native_ok, dehaze_batch
 
     native = _native_ok(params, H, W)
     eng = engine_for(dev)
-    out = torch.empty_like(frames)
+    out = torch.empty((n, OH, OW, 3), dtype=torch.uint8, device=dev)
     air = torch.empty((n, 3), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
     n_ev = 5
@@ -305,7 +330,14 @@ def main():
     pipe_bytes = ALG_BYTES[cfg] * n * npx
     pipe_gbs = pipe_bytes / (ms_step / 1000.0) / 1e9
     traffic_px = _ncu_traffic_per_px()
-    if native and params.mode == "video":
+    if native and (OH, OW) != (H, W):
+        rec_bytes = n * (3 * npx + 3 * OH * OW)   # R3: read I (3 B/input px), write O (3 B/output px)
+        rec_gbs = rec_bytes / (stage_ms[3] / 1000.0) / 1e9
+        roof = {"bound": "hbm", "kernel": "k_rs_recover (R3, resize + recovery, fp64)", "achieved": round(rec_gbs, 1),
+                "peak": peak, "unit": "GB/s", "frac": round(rec_gbs / peak, 4), "traffic": None,
+                "peak_kind": peak_kind, "alg_bytes_per_launch": rec_bytes, "launch_ms": round(stage_ms[3], 4)}
+        launches = 3 + (2 if params.balance_enabled() else 0)
+    elif native and params.mode == "video":
         rec_bytes = 6 * n * npx          # K6: read I (3 B/px), write O (3 B/px)
         rec_gbs = rec_bytes / (stage_ms[3] / 1000.0) / 1e9
         t_px = traffic_px.get("k_recover_lut")
@@ -335,7 +367,7 @@ def main():
     if args.e2e_steps > 0:
         host_in = torch.empty((n, H, W, 3), dtype=torch.uint8, pin_memory=True)
         host_in.copy_(frames)
-        host_out = torch.empty_like(host_in, pin_memory=True)
+        host_out = torch.empty((n, OH, OW, 3), dtype=torch.uint8, pin_memory=True)
         host_air = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
         dehaze_host_batch(host_in, params, out=host_out, airlight=host_air)   # warm-up
         torch.cuda.synchronize()
@@ -377,9 +409,10 @@ def main():
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": ("u8" if params.mode == "video" else "u8 in/out, f64 guided filter") if native else "f64",
+            "dtype": ("f64 (resized image)" if (OH, OW) != (H, W) else
+                      "u8" if params.mode == "video" else "u8 in/out, f64 guided filter") if native else "f64",
             "data": "synthetic (seeded BASELINE generator, generated on device)",
-            "config": {"workload": f"{cfg}: {n} frames {W}x{H} per GPU, {params.mode} mode, native resolution"
+            "config": {"workload": f"{cfg}: {n} frames {W}x{H} per GPU, {params.mode} mode, " + _size_note(params)
                                    + (", gray-world balance" if params.balance_enabled() else ""),
                        "frames_per_gpu": n, "fps": round(n * world / (ms_step / 1000.0), 1),
                        "l2": f"inputs {n * 3 * npx / 1e9:.2f} GB/step > 126 MB L2 (no flush needed)",

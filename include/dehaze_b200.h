@@ -85,9 +85,29 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int height, int width
 /* Byte offsets inside the workspace after dhz_frames_u8 returned (valid until the
  * workspace is reused): [0] dark map u8 (n x H*W, frame stride [1]),
  * [2] selected airlight pixel indices uint32 (n x K, in summation order),
- * [3] transmission map (image mode: float64, n x H*W; video mode: unused, -1),
+ * [3] image mode: guided-filter scratch (fp64 a, b maps of the last frame chunk);
+ *     video mode: -1,
  * [4] total workspace bytes. */
 int dhz_frames_u8_layout(int n, int height, int width, const dhz_params* p, int64_t* offsets5);
+
+/* ---------------------------------------------------------------------------
+ * Default video mode: the same stages with the frames first resized from
+ * h x w to height x width (resize_to) by the reference's pixel-centre bilinear
+ * filter in float64 (imageops.py:47-78, pipeline.py:175-180).  Replaces
+ * dehaze_frame / process_stream with DehazeParams() (resize_to=(640, 480)) on
+ * non-640x480 input.  p->mode must be 0 and p->top_k refers to height*width;
+ * patch_radius <= 32.  out: n frames height x width x 3 u8.  Events as above
+ * ([3] == [2]: no separate transmission stage).
+ * ------------------------------------------------------------------------- */
+size_t dhz_frames_resize_u8_workspace(int n, int h, int w, int height, int width, const dhz_params* p);
+int dhz_frames_resize_u8(const uint8_t* in, int64_t in_fs, int n, int h, int w, int height, int width,
+                         const dhz_params* p, uint8_t* out, int64_t out_fs, double* airlight, void* ws,
+                         size_t ws_bytes, void* stream, void* const* events);
+/* Offsets after dhz_frames_resize_u8: [0] dark map float64 (n x height*width,
+ * frame stride [1] bytes), [2] selected indices uint32 (n x K, summation order),
+ * [3] -1, [4] total workspace bytes. */
+int dhz_frames_resize_u8_layout(int n, int h, int w, int height, int width, const dhz_params* p,
+                                int64_t* offsets5);
 
 /* ---------------------------------------------------------------------------
  * float64 stage operations (reference public functions on float64 arrays; one

@@ -60,6 +60,11 @@ SIGNATURES = {
     "dhz_frames_u8": (_c_int, [_c_void_p, _c_i64, _c_int, _c_int, _c_int, _P, _c_void_p, _c_i64,
                                _c_void_p, _c_void_p, _c_size, _c_void_p, _c_void_p]),
     "dhz_frames_u8_layout": (_c_int, [_c_int, _c_int, _c_int, _P, ctypes.POINTER(_c_i64)]),
+    "dhz_frames_resize_u8_workspace": (_c_size, [_c_int, _c_int, _c_int, _c_int, _c_int, _P]),
+    "dhz_frames_resize_u8": (_c_int, [_c_void_p, _c_i64, _c_int, _c_int, _c_int, _c_int, _c_int, _P, _c_void_p,
+                                      _c_i64, _c_void_p, _c_void_p, _c_size, _c_void_p, _c_void_p]),
+    "dhz_frames_resize_u8_layout": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _P,
+                                             ctypes.POINTER(_c_i64)]),
     # float64 stage operations
     "dhz_f64_stats": (_c_int, [_c_void_p, _c_i64, _c_void_p, _c_void_p, _c_void_p]),
     "dhz_u8_to_f64": (_c_int, [_c_void_p, _c_i64, _c_void_p, _c_void_p]),

@@ -195,4 +195,111 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const d
   return DHZ_OK;
 }
 
+/* ----------------------------------------------------------- resize path ---- */
+
+namespace {
+
+struct RLayout {
+  int64_t hist, zero_end, sel, bal, dark, total, dark_fs;
+};
+
+RLayout make_rlayout(int n, int H, int W, const dhz_params* p) {
+  RLayout L{};
+  const int64_t npx = (int64_t)H * W;
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t at = o;
+    o = align_up(o + bytes);
+    return at;
+  };
+  L.hist = take(4LL * dhz::kResizeBuckets * n);
+  L.zero_end = o;
+  L.sel = take(4LL * n * std::max<int64_t>(1, p->top_k));
+  L.bal = p->balance ? take((int64_t)dhz::resize_balance_ws_bytes(n)) : -1;
+  L.dark_fs = 8 * npx;
+  L.dark = take(L.dark_fs * n);
+  L.total = o;
+  return L;
+}
+
+int check_resize(int n, int h, int w, int H, int W, const dhz_params* p) {
+  int rc = check_params(n, H, W, p);
+  if (rc) return rc;
+  if (h < 1 || w < 1) return fail(DHZ_E_INVALID, "empty source frame %dx%d", w, h);
+  if ((int64_t)h * w > 0x7FFFFFFFLL) return fail(DHZ_E_INVALID, "source frame too large");
+  if (p->mode != 0) return fail(DHZ_E_UNSUPPORTED, "the resize path runs video mode only");
+  if (p->patch_radius > dhz::kResizeMaxRadius)
+    return fail(DHZ_E_UNSUPPORTED, "patch_radius %d above %d on the resize path", p->patch_radius,
+                dhz::kResizeMaxRadius);
+  return DHZ_OK;
+}
+
+dhz::ResizeGeo make_geo(int h, int w, int H, int W) {
+  dhz::ResizeGeo g;
+  g.h = h;
+  g.w = w;
+  g.H = H;
+  g.W = W;
+  g.sy = (double)h / (double)H;  // pipeline/imageops: h / height, w / width (IEEE division)
+  g.sx = (double)w / (double)W;
+  return g;
+}
+
+}  // namespace
+
+size_t dhz_frames_resize_u8_workspace(int n, int h, int w, int height, int width, const dhz_params* p) {
+  if (check_resize(std::max(n, 0), h, w, height, width, p) != DHZ_OK) return 0;
+  return (size_t)make_rlayout(n, height, width, p).total;
+}
+
+int dhz_frames_resize_u8_layout(int n, int h, int w, int height, int width, const dhz_params* p, int64_t* off) {
+  int rc = check_resize(n, h, w, height, width, p);
+  if (rc) return rc;
+  if (!off) return fail(DHZ_E_INVALID, "offsets is NULL");
+  const RLayout L = make_rlayout(n, height, width, p);
+  off[0] = L.dark;
+  off[1] = L.dark_fs;
+  off[2] = L.sel;
+  off[3] = -1;
+  off[4] = L.total;
+  return DHZ_OK;
+}
+
+int dhz_frames_resize_u8(const uint8_t* in, int64_t in_fs, int n, int h, int w, int H, int W, const dhz_params* p,
+                         uint8_t* out, int64_t out_fs, double* airlight, void* ws, size_t ws_bytes, void* stream,
+                         void* const* events) {
+  int rc = check_resize(n, h, w, H, W, p);
+  if (rc) return rc;
+  if (n == 0) return DHZ_OK;
+  if (!in || !out || !airlight) return fail(DHZ_E_INVALID, "NULL array argument");
+  if (in_fs < 3LL * h * w || out_fs < 3LL * H * W) return fail(DHZ_E_INVALID, "frame stride smaller than a frame");
+  const RLayout L = make_rlayout(n, H, W, p);
+  if (!ws || (int64_t)ws_bytes < L.total)
+    return fail(DHZ_E_WORKSPACE, "workspace too small: need %lld bytes, got %zu", (long long)L.total, ws_bytes);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  auto mark = [&](int i) {
+    if (events && events[i]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[i]), st);
+  };
+  const dhz::ResizeGeo g = make_geo(h, w, H, W);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  double* dark = reinterpret_cast<double*>(base + L.dark);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(base + L.hist);
+  uint32_t* sel = reinterpret_cast<uint32_t*>(base + L.sel);
+  mark(0);
+  cudaError_t e = cudaMemsetAsync(base, 0, (size_t)L.zero_end, st);
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  e = dhz::resize_dark(in, in_fs, n, g, p->patch_radius, dark, hist, st);
+  if (e != cudaSuccess) return cuda_fail(e, "resize_dark");
+  mark(1);
+  e = dhz::resize_select(in, in_fs, n, g, dark, hist, p->top_k, p->alpha, sel, airlight, st);
+  if (e != cudaSuccess) return cuda_fail(e, "resize_select");
+  mark(2);
+  mark(3);
+  e = dhz::resize_recover(in, in_fs, n, g, airlight, p->omega, p->t_min, p->thresholds, p->gamma, p->balance != 0,
+                          p->balance ? base + L.bal : nullptr, out, out_fs, st);
+  if (e != cudaSuccess) return cuda_fail(e, "resize_recover");
+  mark(4);
+  return DHZ_OK;
+}
+
 }  // extern "C"

@@ -212,4 +212,50 @@ __device__ __forceinline__ int quantize_unit(double y) {
   return (int)floor(z);
 }
 
+// Correctly rounded a / b from rb = RN(1/b): q0 = RN(a*rb) lies within 1 ulp of
+// a/b, the FMA residual a - b*q0 is exact, and one correction step rounds to
+// RN(a/b) (Markstein's theorem; b is a positive normal number here).
+__device__ __forceinline__ double div_rb(double a, double b, double rb) {
+  const double q = __dmul_rn(a, rb);
+  const double r = __fma_rn(-q, b, a);
+  return __fma_rn(r, rb, q);
+}
+
+// x^e for x in [0, 1], e > 0, to a few ulp (exp(e*log(x)) with a 2*atanh
+// series for the log and a degree-13 Taylor exp) — used only inside the
+// gray-world channel sums, where per-sample errors of ~1e-16 are far below the
+// reference's own summation rounding.  Bytes are never derived from it.
+__device__ __forceinline__ double pow_unit(double x, double e) {
+  if (!(x >= 0x1p-1000)) return 0.0;  // (recovered values are 0 or far above this)
+  if (x >= 1.0) return 1.0;
+  const long long bits = __double_as_longlong(x);
+  int ex = (int)(bits >> 52) - 1022;                                           // x = m * 2^ex
+  double m = __longlong_as_double((bits & 0x000fffffffffffffLL) | 0x3fe0000000000000LL);  // m in [0.5, 1)
+  if (m < 0.70710678118654752) { m = m * 2.0; ex -= 1; }   // m in [sqrt(1/2), sqrt(2))
+  const double s = (m - 1.0) * __drcp_rn(m + 1.0);
+  const double s2 = s * s;
+  double p = 1.0 / 23;
+  p = fma(p, s2, 1.0 / 21); p = fma(p, s2, 1.0 / 19); p = fma(p, s2, 1.0 / 17); p = fma(p, s2, 1.0 / 15);
+  p = fma(p, s2, 1.0 / 13); p = fma(p, s2, 1.0 / 11); p = fma(p, s2, 1.0 / 9);  p = fma(p, s2, 1.0 / 7);
+  p = fma(p, s2, 1.0 / 5);  p = fma(p, s2, 1.0 / 3);
+  const double lnm = 2.0 * fma(p * s2, s, s);  // 2 atanh(s) = ln(m)
+  constexpr double kLn2Hi = 6.93147180369123816490e-01, kLn2Lo = 1.90821492927058770002e-10;
+  const double y = e * fma((double)ex, kLn2Hi, fma((double)ex, kLn2Lo, lnm));   // e * ln(x) <= 0
+  if (y < -700.0) return 0.0;  // keeps 2^k normal below
+  const double k = rint(y * 1.44269504088896340736);
+  const double r = fma(-k, kLn2Lo, fma(-k, kLn2Hi, y));  // |r| <= ~0.35
+  double q = 1.0 / 6227020800.0;                          // 1/13!
+  q = fma(q, r, 1.0 / 479001600.0); q = fma(q, r, 1.0 / 39916800.0); q = fma(q, r, 1.0 / 3628800.0);
+  q = fma(q, r, 1.0 / 362880.0);    q = fma(q, r, 1.0 / 40320.0);    q = fma(q, r, 1.0 / 5040.0);
+  q = fma(q, r, 1.0 / 720.0);       q = fma(q, r, 1.0 / 120.0);      q = fma(q, r, 1.0 / 24.0);
+  q = fma(q, r, 1.0 / 6.0);         q = fma(q, r, 0.5);              q = fma(q, r, 1.0);
+  q = fma(q, r, 1.0);
+  return q * __longlong_as_double((long long)((int)k + 1023) << 52);  // k in [-1010, 0]
+}
+
+// clip(((v/255 - A) / t) + A, 0, 1) with the division done as div_rb(., t, RN(1/t)).
+__device__ __forceinline__ double recover_x(double x, double A, double t, double rt) {
+  return fmin(fmax(__dadd_rn(div_rb(__dsub_rn(x, A), t, rt), A), 0.0), 1.0);
+}
+
 }  // namespace dhz

@@ -58,6 +58,33 @@ cudaError_t guided_recover_u8(const uint8_t* in, int64_t in_fs, int n, int H, in
                               const double* airlight, double omega, double t_min, const double* thr, double gamma,
                               bool balance, uint8_t* out, int64_t out_fs, void* ws, cudaStream_t st);
 
+// Gray-world balance from per-CTA channel sums of the gamma values (part[n][nparts][3]):
+// per frame and channel the gains and the 256 exact byte thresholds on the recovered
+// value (thr[n][3][256], thr[.][.][0] = -1, +inf for unreachable levels); gains[n][3]
+// (fp32) only seed the threshold walk.
+cudaError_t balance_thresholds(const double* part, int nparts, int n, int64_t npx, double gamma, double* thr,
+                               float* gains, cudaStream_t st);
+
+// Default video mode: frames resized (fp64 bilinear, recomputed from the u8 input
+// wherever needed) and dehazed at the working size (resize_u8.cu).
+constexpr int kResizeMaxRadius = 32;
+constexpr int kResizeBuckets = 4097;  // floor(dark * 4096) for dark in [0, 1]
+constexpr int kResizeSumParts = 64;   // CTAs per frame of the balance sums pass
+struct ResizeGeo {
+  int h, w;        // source frame
+  int H, W;        // working size (resize_to)
+  double sy, sx;   // h / H, w / W (the reference's Python float divisions)
+};
+cudaError_t resize_dark(const uint8_t* in, int64_t in_fs, int n, const ResizeGeo& g, int r, double* dark,
+                        uint32_t* hist /* [n][kResizeBuckets], zeroed by the caller */, cudaStream_t st);
+cudaError_t resize_select(const uint8_t* in, int64_t in_fs, int n, const ResizeGeo& g, const double* dark,
+                          const uint32_t* hist, int64_t K, double alpha, uint32_t* sel /* [n][K] */,
+                          double* airlight, cudaStream_t st);
+size_t resize_balance_ws_bytes(int n);
+cudaError_t resize_recover(const uint8_t* in, int64_t in_fs, int n, const ResizeGeo& g, const double* airlight,
+                           double omega, double t_min, const double* thr, double gamma, bool balance,
+                           void* bal_ws, uint8_t* out, int64_t out_fs, cudaStream_t st);
+
 // Gray-world balanced LUT (g table, per-frame channel sums, gains); ws: balance_ws_bytes(n).
 size_t balance_ws_bytes(int n);
 cudaError_t build_lut_balanced_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const double* airlight,

@@ -60,27 +60,42 @@ class FrameEngine:
         _native.check(self.lib.dhz_frames_u8_layout(n, H, W, ctypes.byref(p), off), "dhz_frames_u8_layout")
         return list(off)
 
+    @staticmethod
+    def working_size(params, H, W):
+        """(height, width) the pipeline runs at: resize_to, or the native size."""
+        if params.resize_to is None:
+            return H, W
+        rw, rh = (int(v) for v in params.resize_to)
+        return rh, rw
+
     def run(self, frames: torch.Tensor, params, out: torch.Tensor | None = None,
             airlight: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None,
             keep_maps: bool = False, events=None):
         """Dehaze ``frames`` (n, H, W, 3) uint8 CUDA, C-contiguous.
 
-        Returns (out uint8 (n, H, W, 3), airlight float64 (n, 3)) as CUDA tensors,
-        plus a dict of device maps when ``keep_maps`` (dark u8, selected indices).
+        Frames are first resized to ``params.resize_to`` when that differs from
+        their size (video mode, dhz_frames_resize_u8).  Returns (out uint8
+        (n, H', W', 3), airlight float64 (n, 3)) as CUDA tensors, plus a dict of
+        device maps when ``keep_maps`` (dark map — u8 at native size, float64
+        after a resize — and the selected indices).
         """
         if frames.dim() != 4 or frames.shape[-1] != 3 or frames.dtype != torch.uint8:
             raise ValueError(f"frames must be (n, H, W, 3) uint8, got {tuple(frames.shape)} {frames.dtype}")
         if not frames.is_cuda:
             raise ValueError("frames must be a CUDA tensor")
         frames = frames.contiguous()
-        n, H, W, _ = frames.shape
+        n, h, w, _ = frames.shape
+        H, W = self.working_size(params, h, w)
+        resize = (H, W) != (h, w)
         dev = frames.device
         thr = device_thresholds(params.gamma, dev)
         p = native_params(params, H * W, thr)
         if out is None:
-            out = torch.empty_like(frames)
+            out = torch.empty((n, H, W, 3), dtype=torch.uint8, device=dev)
         if airlight is None:
             airlight = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        if n == 0:
+            return (out, airlight, {}) if keep_maps else (out, airlight)
         st = stream if stream is not None else torch.cuda.current_stream(dev)
         ev_arr = None
         if events is not None:
@@ -90,22 +105,39 @@ class FrameEngine:
                 ev.record(st)
             ev_arr = (ctypes.c_void_p * len(events))(*[ev.cuda_event for ev in events])
         with self._lock:
-            nbytes = self.lib.dhz_frames_u8_workspace(n, H, W, ctypes.byref(p))
-            if nbytes == 0:
-                _native.check(_native.DHZ_E_INVALID, "dhz_frames_u8_workspace")
-            ws = self.workspace(nbytes)
-            rc = self.lib.dhz_frames_u8(
-                frames.data_ptr(), 3 * H * W, n, H, W, ctypes.byref(p), out.data_ptr(), 3 * H * W,
-                airlight.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream, ev_arr)
-            _native.check(rc, "dhz_frames_u8")
+            if resize:
+                nbytes = self.lib.dhz_frames_resize_u8_workspace(n, h, w, H, W, ctypes.byref(p))
+                if nbytes == 0:
+                    _native.check(_native.DHZ_E_INVALID, "dhz_frames_resize_u8_workspace")
+                ws = self.workspace(nbytes)
+                rc = self.lib.dhz_frames_resize_u8(
+                    frames.data_ptr(), 3 * h * w, n, h, w, H, W, ctypes.byref(p), out.data_ptr(), 3 * H * W,
+                    airlight.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream, ev_arr)
+                _native.check(rc, "dhz_frames_resize_u8")
+            else:
+                nbytes = self.lib.dhz_frames_u8_workspace(n, H, W, ctypes.byref(p))
+                if nbytes == 0:
+                    _native.check(_native.DHZ_E_INVALID, "dhz_frames_u8_workspace")
+                ws = self.workspace(nbytes)
+                rc = self.lib.dhz_frames_u8(
+                    frames.data_ptr(), 3 * H * W, n, H, W, ctypes.byref(p), out.data_ptr(), 3 * H * W,
+                    airlight.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream, ev_arr)
+                _native.check(rc, "dhz_frames_u8")
             maps = None
             if keep_maps:
-                off = self.layout(n, H, W, p)
-                dark_fs = off[1]
-                dark = ws[off[0]: off[0] + dark_fs * n].view(n, dark_fs)[:, : H * W].reshape(n, H, W).clone()
                 k = p.top_k
-                sel = ws[off[2]: off[2] + 4 * n * k].view(torch.int32).view(n, k).clone()
-                maps = {"dark_u8": dark, "selected": sel}
+                if resize:
+                    off = (ctypes.c_int64 * 5)()
+                    _native.check(self.lib.dhz_frames_resize_u8_layout(n, h, w, H, W, ctypes.byref(p), off),
+                                  "dhz_frames_resize_u8_layout")
+                    dark = ws[off[0]: off[0] + off[1] * n].view(torch.float64).view(n, H, W).clone()
+                    maps = {"dark_f64": dark}
+                else:
+                    off = self.layout(n, H, W, p)
+                    dark_fs = off[1]
+                    dark = ws[off[0]: off[0] + dark_fs * n].view(n, dark_fs)[:, : H * W].reshape(n, H, W).clone()
+                    maps = {"dark_u8": dark}
+                maps["selected"] = ws[off[2]: off[2] + 4 * n * k].view(torch.int32).view(n, k).clone()
         if keep_maps:
             return out, airlight, maps
         return out, airlight

@@ -186,13 +186,17 @@ def _needs_resize(params, h, w):
 GUIDED_MAX_RADIUS = 255  # dhz::kGuidedMaxRadius (fused guided filter: 2r < 512 columns per strip)
 
 
+RESIZE_MAX_RADIUS = 32  # dhz::kResizeMaxRadius (tile halo of the resize path's erosion)
+
+
 def _native_ok(params, h, w, want_maps=False):
-    """The fused u8 batch pipeline covers both modes at the working size (with or
-    without gray-world balance).  The resize path, guided radii above
-    GUIDED_MAX_RADIUS and image-mode map capture (the fused kernels never
-    materialise t~ for every pixel) use the float64 device path."""
+    """Whether the batched native pipeline (dhz_frames_u8 / dhz_frames_resize_u8)
+    covers this call: video mode at native size or resized (patch radius up to
+    RESIZE_MAX_RADIUS), image mode at native size (guided radius up to
+    GUIDED_MAX_RADIUS).  Map capture outside plain native-size video, image mode
+    with a resize, and larger radii use the per-frame float64 device path."""
     if _needs_resize(params, h, w):
-        return False
+        return params.mode == "video" and int(params.patch_radius) <= RESIZE_MAX_RADIUS and not want_maps
     if params.mode == "image":
         return int(params.guided_radius) <= GUIDED_MAX_RADIUS and not want_maps
     return True
@@ -287,7 +291,9 @@ def dehaze_batch(frames, params=None, out=None):
     """Dehaze a device-resident batch (n, H, W, 3) uint8 CUDA tensor in one pipeline launch.
 
     Returns (out, airlight) CUDA tensors: out (n, H', W', 3) uint8, airlight
-    (n, 3) float64.  Frames that need a resize go through the float path.
+    (n, 3) float64, with (H', W') the working size (resize_to in video mode).
+    Calls the batched native path does not cover (see _native_ok) run the
+    per-frame float64 device path.
     """
     if params is None:
         params = DehazeParams()
@@ -316,7 +322,7 @@ def dehaze_batch(frames, params=None, out=None):
 class _HostPipe:
     """Per-(device, shape) ring of stream slots for host-resident batches."""
 
-    def __init__(self, dev, chunk, H, W, slots=3):
+    def __init__(self, dev, chunk, H, W, OH, OW, slots=3):
         import torch
 
         from .engine import FrameEngine
@@ -324,7 +330,7 @@ class _HostPipe:
         self.streams = [torch.cuda.Stream(dev) for _ in range(slots)]
         self.engines = [FrameEngine(dev) for _ in range(slots)]
         self.din = [torch.empty((chunk, H, W, 3), dtype=torch.uint8, device=dev) for _ in range(slots)]
-        self.dout = [torch.empty((chunk, H, W, 3), dtype=torch.uint8, device=dev) for _ in range(slots)]
+        self.dout = [torch.empty((chunk, OH, OW, 3), dtype=torch.uint8, device=dev) for _ in range(slots)]
         self.dair = [torch.empty((chunk, 3), dtype=torch.float64, device=dev) for _ in range(slots)]
 
 
@@ -336,8 +342,8 @@ def dehaze_host_batch(frames, params=None, out=None, airlight=None, chunk=None):
 
     Frames move to the GPU in chunks on a ring of streams: H2D copy, fused
     pipeline and D2H copy of chunk c overlap those of chunks c-1 and c+1.
-    Returns (out, airlight) host tensors (pinned when allocated here).
-    Native-size frames only (the resize path is per-frame float64).
+    Returns (out, airlight) host tensors (pinned when allocated here); out has
+    the working size (resize_to in video mode).
     """
     import torch
 
@@ -356,18 +362,21 @@ def dehaze_host_batch(frames, params=None, out=None, airlight=None, chunk=None):
             a = airlight
         return o.cpu() if o.is_cuda else o, a.cpu() if a.is_cuda else a
     dev = _device()
+    from .engine import FrameEngine
+
+    OH, OW = FrameEngine.working_size(params, H, W)
     if out is None:
-        out = torch.empty((n, H, W, 3), dtype=torch.uint8, pin_memory=True)
+        out = torch.empty((n, OH, OW, 3), dtype=torch.uint8, pin_memory=True)
     if airlight is None:
         airlight = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
     if n == 0:
         return out, airlight
     if chunk is None:
         chunk = max(1, min(n, (48 << 20) // (3 * H * W)))
-    key = (dev.index, chunk, H, W)
+    key = (dev.index, chunk, H, W, OH, OW)
     pipe = _host_pipes.get(key)
     if pipe is None:
-        pipe = _host_pipes[key] = _HostPipe(dev, chunk, H, W)
+        pipe = _host_pipes[key] = _HostPipe(dev, chunk, H, W, OH, OW)
     cur = torch.cuda.current_stream(dev)
     for st in pipe.streams:
         st.wait_stream(cur)

@@ -68,10 +68,10 @@ def test_stage_functions():
     assert np.array_equal(dz.resize_bilinear(img, 30, 25), s["resize_up"])
 
 
-@pytest.mark.parametrize("name", sorted(n for n in CASES if CASES[n]["params"].get("mode") == "image"))
-def test_pipeline_case_fused_image(name):
-    """Image mode without map capture runs the fused u8 guided-filter path
-    (guided_u8.cu) — same output bar as above."""
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_pipeline_case_batched(name):
+    """Without map capture the batched native kernels run (dhz_frames_u8: video and
+    image mode at native size; dhz_frames_resize_u8: default resize) — same bars."""
     from paper_2512_16609_b200 import FrameTelemetry, dehaze_frame, pipeline
 
     c = CASES[name]
@@ -79,9 +79,10 @@ def test_pipeline_case_fused_image(name):
     total_mismatch = 0
     for i, f in enumerate(c["frames"]):
         h, w = f.shape[:2]
-        assert pipeline._native_ok(p, h, w) or pipeline._needs_resize(p, h, w)
+        assert pipeline._native_ok(p, h, w)
         tel = FrameTelemetry()
         out = dehaze_frame(f, p, tel)
+        assert out.shape == c["out"][i].shape
         assert np.abs(tel.airlights[0] - c["airlight"][i]).max() <= 1e-12
         d = np.abs(out.astype(np.int16) - c["out"][i].astype(np.int16))
         assert d.max() <= 1
