@@ -340,8 +340,8 @@ def main():
     elif native and params.mode == "video":
         rec_bytes = 6 * n * npx          # K6: read I (3 B/px), write O (3 B/px)
         rec_gbs = rec_bytes / (stage_ms[3] / 1000.0) / 1e9
-        t_px = traffic_px.get("k_recover_lut")
-        roof = {"bound": "hbm", "kernel": "k_recover_lut (K6, LUT recovery)", "achieved": round(rec_gbs, 1),
+        t_px = traffic_px.get("k_recover_lut_diag")
+        roof = {"bound": "hbm", "kernel": "k_recover_lut_diag (K6, LUT recovery)", "achieved": round(rec_gbs, 1),
                 "peak": peak, "unit": "GB/s", "frac": round(rec_gbs / peak, 4),
                 "traffic": None if t_px is None else int(t_px * n * npx), "peak_kind": peak_kind,
                 "alg_bytes_per_launch": rec_bytes, "launch_ms": round(stage_ms[3], 4),
