@@ -96,17 +96,28 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
   // ---------------- pass 1: channel min + horizontal min, warp per row ----------------
   const int x = x0 - 16 + 16 * lane;  // first pixel of this lane
   const bool col_ok = x >= 0 && x < W;  // W % 16 == 0: a 16-px unit is fully in or out
-  for (int v = warp; v < G::ROWS; v += kThreads / 32) {
+  // register double buffering: row v+8's three 128-bit loads are in flight while
+  // row v is reduced (the loop is otherwise bound by the load latency)
+  auto load_row = [&](int v, uint4& a, uint4& b, uint4& d) {
     const int y = y0 - R + v;
-    uint32_t c[8];
-    if (y >= 0 && y < H && col_ok) {
+    if (v < G::ROWS && y >= 0 && y < H && col_ok) {
       const uint8_t* src = frame + ((int64_t)y * W + x) * 3;
-      const uint4 a = ldg_nc_v4(src), b = ldg_nc_v4(src + 16), d = ldg_nc_v4(src + 32);
-      const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
-      cmin16_pairs(w, c);
+      a = ldg_nc_v4(src);
+      b = ldg_nc_v4(src + 16);
+      d = ldg_nc_v4(src + 32);
     } else {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) c[k] = 0xFFFFFFFFu;
+      a = b = d = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    }
+  };
+  uint4 na, nb, nd;
+  load_row(warp, na, nb, nd);
+  for (int v = warp; v < G::ROWS; v += kThreads / 32) {
+    const uint4 a = na, b = nb, d = nd;
+    load_row(v + kThreads / 32, na, nb, nd);
+    uint32_t c[8];
+    {
+      const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
+      cmin16_pairs(w, c);  // all-ones words (outside the frame) stay all-ones
     }
     // local pairs: [HPR from the left lane][8 own][HPR from the right lane][pad]
     uint32_t m[NP];
