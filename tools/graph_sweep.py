@@ -31,7 +31,9 @@ def bench(fn, iters=10):
     return e0.elapsed_time(e1) / iters
 
 
-for S, C in [(1, n), (2, 4), (2, 8), (2, 16), (2, 32), (3, 4), (3, 8), (4, 4), (4, 8)]:
+CASES = [tuple(int(v) for v in c.split("x")) for c in os.environ.get("CASES", "").split(",") if c] or \
+    [(1, n), (2, 4), (2, 8), (2, 16), (2, 32), (3, 4), (3, 8), (4, 4), (4, 8)]
+for S, C in CASES:
     gp = GraphedPipeline(frames, params, streams=S, chunk=C)
     ms = bench(gp.replay)
     ok = torch.equal(gp.out, ref_out) and torch.equal(gp.airlight, ref_air)
