@@ -110,8 +110,9 @@ k_gf_pass1(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
            double* __restrict__ b_out) {
   constexpr int NC = kThreads * CPT;
   __shared__ GuideTables T;
-  __shared__ double pre[2][4][NC + 1];
+  extern __shared__ double dyn_pre[];  // [2 buffers][4 sums][NC + 1] prefix rows
   __shared__ double wt[2][4][kThreads / 32];
+  auto pre = [&](int buf, int q) { return dyn_pre + (buf * 4 + q) * (NC + 1); };
   const int f = blockIdx.z;
   const int sw = NC - 2 * r;                     // output columns of this strip
   const int x0 = blockIdx.x * sw;                // first output column
@@ -124,7 +125,7 @@ k_gf_pass1(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
     load_guide(T, v, x);
     T.t[v] = fmin(fmax(__dsub_rn(1.0, __dmul_rn(omega, __ddiv_rn(x, amax))), t_min), 1.0);
   }
-  if (threadIdx.x < 8) pre[threadIdx.x >> 2][threadIdx.x & 3][0] = 0.0;
+  if (threadIdx.x < 8) pre(threadIdx.x >> 2, threadIdx.x & 3)[0] = 0.0;
   __syncthreads();
   const uint8_t* frame = in + (int64_t)f * in_fs;
   const int64_t pitch = 3LL * W;
@@ -182,7 +183,7 @@ k_gf_pass1(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
 #pragma unroll
       for (int k = 0; k < CPT; ++k) {
         run = __dadd_rn(run, s[q][k]);
-        pre[buf][q][threadIdx.x * CPT + k + 1] = run;
+        pre(buf, q)[threadIdx.x * CPT + k + 1] = run;
       }
     }
     __syncthreads();
@@ -193,10 +194,10 @@ k_gf_pass1(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
       if (j < sw && x0 + j < W) {
         // window over strip input columns [j, j + 2r] = prefix[j+2r+1] - prefix[j]
         const int hi = j + 2 * r + 1;
-        const double mi = div_rb(__dsub_rn(pre[buf][0][hi], pre[buf][0][j]), kk, rkk);
-        const double mp = div_rb(__dsub_rn(pre[buf][1][hi], pre[buf][1][j]), kk, rkk);
-        const double cip = div_rb(__dsub_rn(pre[buf][2][hi], pre[buf][2][j]), kk, rkk);
-        const double cii = div_rb(__dsub_rn(pre[buf][3][hi], pre[buf][3][j]), kk, rkk);
+        const double mi = div_rb(__dsub_rn(pre(buf, 0)[hi], pre(buf, 0)[j]), kk, rkk);
+        const double mp = div_rb(__dsub_rn(pre(buf, 1)[hi], pre(buf, 1)[j]), kk, rkk);
+        const double cip = div_rb(__dsub_rn(pre(buf, 2)[hi], pre(buf, 2)[j]), kk, rkk);
+        const double cii = div_rb(__dsub_rn(pre(buf, 3)[hi], pre(buf, 3)[j]), kk, rkk);
         const double var = __dsub_rn(cii, __dmul_rn(mi, mi));
         const double cov = __dsub_rn(cip, __dmul_rn(mi, mp));
         const double av = __ddiv_rn(cov, __dadd_rn(var, eps));
@@ -223,8 +224,9 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
   constexpr int NC = kThreads * CPT;
   __shared__ GuideTables T;  // wr/wg/wb for the guide; t[] holds v/255 here
   __shared__ double sA[3], s_thr[256];
-  __shared__ double pre[2][2][NC + 1];
+  extern __shared__ double dyn_pre[];  // [2 buffers][2 sums][NC + 1] prefix rows
   __shared__ double wt[2][2][kThreads / 32];
+  auto pre = [&](int buf, int q) { return dyn_pre + (buf * 2 + q) * (NC + 1); };
   const int f = blockIdx.z;
   const int sw = NC - 2 * r;
   const int x0 = blockIdx.x * sw;
@@ -238,7 +240,7 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
     s_thr[v] = thr[v];
   }
   if (threadIdx.x < 3) sA[threadIdx.x] = airlight[3 * f + threadIdx.x];
-  if (threadIdx.x < 4) pre[threadIdx.x >> 1][threadIdx.x & 1][0] = 0.0;
+  if (threadIdx.x < 4) pre(threadIdx.x >> 1, threadIdx.x & 1)[0] = 0.0;
   __syncthreads();
   int xc[CPT];
 #pragma unroll
@@ -283,8 +285,8 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
       for (int k = 0; k < CPT; ++k) {
         ra = __dadd_rn(ra, sa[k]);
         rb = __dadd_rn(rb, sb[k]);
-        pre[buf][0][threadIdx.x * CPT + k + 1] = ra;
-        pre[buf][1][threadIdx.x * CPT + k + 1] = rb;
+        pre(buf, 0)[threadIdx.x * CPT + k + 1] = ra;
+        pre(buf, 1)[threadIdx.x * CPT + k + 1] = rb;
       }
     }
     __syncthreads();
@@ -293,8 +295,8 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
       const int j = k * kThreads + (int)threadIdx.x;
       if (j < sw && x0 + j < W) {
         const int hi = j + 2 * r + 1;
-        const double ma = div_rb(__dsub_rn(pre[buf][0][hi], pre[buf][0][j]), kk, rkk);
-        const double mb = div_rb(__dsub_rn(pre[buf][1][hi], pre[buf][1][j]), kk, rkk);
+        const double ma = div_rb(__dsub_rn(pre(buf, 0)[hi], pre(buf, 0)[j]), kk, rkk);
+        const double mb = div_rb(__dsub_rn(pre(buf, 1)[hi], pre(buf, 1)[j]), kk, rkk);
         const int64_t pix = (int64_t)y * W + x0 + j;
         const uint8_t* px = frame + pix * 3;
         const uint32_t R = px[0], G = px[1], B = px[2];
@@ -332,7 +334,7 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
 #pragma unroll
       for (int c = 0; c < 3; ++c) v3[c] = __dadd_rn(v3[c], __shfl_xor_sync(0xffffffffu, v3[c], o));
     __syncthreads();  // pre[][] is reused as the cross-warp buffer
-    double* red = &pre[0][0][0];
+    double* red = dyn_pre;
     if ((threadIdx.x & 31) == 0)
       for (int c = 0; c < 3; ++c) red[c * 8 + (threadIdx.x >> 5)] = v3[c];
     __syncthreads();
@@ -448,13 +450,24 @@ k_gf_apply(const uint8_t* __restrict__ in, int64_t in_fs, int64_t npx, const dou
   }
 }
 
-// Columns per thread: 2 (512-column strips) unless that leaves too few CTAs.
+// Columns per thread: the widest strip (4, 2 or 1 columns per thread, i.e.
+// 1024/512/256 input columns) that still leaves >= 2 CTAs per SM; wider strips
+// waste fewer halo columns and amortise the per-row prefix over more columns.
 int guided_cpt(int H, int W, int r, int n) {
-  if (2 * r >= kThreads) return 2;  // only the wide strip fits the window
-  const int sw2 = 2 * kThreads - 2 * r;
-  const int64_t ctas2 = (int64_t)((W + sw2 - 1) / sw2) * n * ((H + 15) / 16);
-  return ctas2 >= 2 * 148 ? 2 : 1;
+  for (int cpt = 4; cpt >= 1; cpt >>= 1) {
+    const int sw = cpt * kThreads - 2 * r;
+    if (sw < 1) return cpt * 2;
+    const int64_t ctas = (int64_t)((W + sw - 1) / sw) * n * ((H + 15) / 16);
+    if (ctas >= 2 * 148 || cpt == 1) {
+      if (2 * r >= cpt * kThreads) return cpt * 2;
+      return cpt;
+    }
+  }
+  return 1;
 }
+
+template <int CPT>
+size_t pass_smem(int nsums) { return (size_t)2 * nsums * (kThreads * CPT + 1) * sizeof(double); }
 
 }  // namespace
 
@@ -488,7 +501,7 @@ size_t guided_ws_bytes(int n, int H, int W, int r, bool balance) {
   size_t b = 16ull * npx * c;                                            // a, b
   if (balance) {
     int64_t parts = 0;
-    for (int cpt = 1; cpt <= 2; ++cpt) {  // either strip width may be chosen for the chunk
+    for (int cpt = 1; cpt <= 4; cpt <<= 1) {  // any strip width may be chosen for the chunk
       const int sw = kThreads * cpt - 2 * r;
       if (sw < 1) continue;
       const int seg = guided_seg_rows(H, W, r, c, cpt);
@@ -520,16 +533,21 @@ cudaError_t guided_recover_u8(const uint8_t* in, int64_t in_fs, int n, int H, in
     double* b = a + npx * c;
     double* t = b + npx * c;
     double* part = t + npx * c;
-    if (cpt == 2) k_gf_pass1<2><<<grid, kThreads, 0, st>>>(fin, in_fs, H, W, r, seg, eps, fA, omega, t_min, a, b);
-    else k_gf_pass1<1><<<grid, kThreads, 0, st>>>(fin, in_fs, H, W, r, seg, eps, fA, omega, t_min, a, b);
+    auto launch = [&](auto k1, auto k2, size_t sm1, size_t sm2) {
+      cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+      cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      k1<<<grid, kThreads, sm1, st>>>(fin, in_fs, H, W, r, seg, eps, fA, omega, t_min, a, b);
+      k2<<<grid, kThreads, sm2, st>>>(fin, in_fs, H, W, r, seg, a, b, fA, t_min, thr, inv_g, g1, fout, out_fs,
+                                      balance ? t : nullptr, balance ? part : nullptr);
+    };
     if (!balance) {
-      auto k2 = cpt == 2 ? k_gf_pass2<0, 2> : k_gf_pass2<0, 1>;
-      k2<<<grid, kThreads, 0, st>>>(fin, in_fs, H, W, r, seg, a, b, fA, t_min, thr, inv_g, g1, fout, out_fs,
-                                    nullptr, nullptr);
+      if (cpt == 4) launch(k_gf_pass1<4>, k_gf_pass2<0, 4>, pass_smem<4>(4), pass_smem<4>(2));
+      else if (cpt == 2) launch(k_gf_pass1<2>, k_gf_pass2<0, 2>, pass_smem<2>(4), pass_smem<2>(2));
+      else launch(k_gf_pass1<1>, k_gf_pass2<0, 1>, pass_smem<1>(4), pass_smem<1>(2));
     } else {
-      auto k2 = cpt == 2 ? k_gf_pass2<1, 2> : k_gf_pass2<1, 1>;
-      k2<<<grid, kThreads, 0, st>>>(fin, in_fs, H, W, r, seg, a, b, fA, t_min, thr, inv_g, g1, fout, out_fs, t,
-                                    part);
+      if (cpt == 4) launch(k_gf_pass1<4>, k_gf_pass2<1, 4>, pass_smem<4>(4), pass_smem<4>(2));
+      else if (cpt == 2) launch(k_gf_pass1<2>, k_gf_pass2<1, 2>, pass_smem<2>(4), pass_smem<2>(2));
+      else launch(k_gf_pass1<1>, k_gf_pass2<1, 1>, pass_smem<1>(4), pass_smem<1>(2));
       const int nparts = grid.x * grid.y;
       double* bthr = part + 3LL * nparts * c;
       float* gains = reinterpret_cast<float*>(bthr + 3LL * 256 * c);
