@@ -27,6 +27,9 @@ constexpr int kTW = kBandW;  // output columns per tile (30 lanes x 16 px)
 constexpr int kBH = 64;    // output rows per tile
 constexpr int kRun = kBandH;  // rows per pass-2 item (== block height of blk_max)
 constexpr int kThreads = 256;
+#ifndef DHZ_K1_MINB
+#define DHZ_K1_MINB 4  // resident CTAs per SM the register budget is sized for
+#endif
 
 template <int R>
 struct RowGeo {
@@ -80,7 +83,7 @@ __device__ __forceinline__ uint32_t vert_final(const uint32_t (&v)[N], int j) {
 }
 
 template <int R>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, DHZ_K1_MINB)
 k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t* __restrict__ dark,
             int64_t dark_fs, uint32_t* __restrict__ frame_max, uint32_t* __restrict__ blk_max) {
   using G = RowGeo<R>;
@@ -98,16 +101,19 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
   const bool col_ok = x >= 0 && x < W;  // W % 16 == 0: a 16-px unit is fully in or out
   // register double buffering: row v+8's three 128-bit loads are in flight while
   // row v is reduced (the loop is otherwise bound by the load latency)
+  // rows advance by 8 per iteration: walk a pointer instead of recomputing y*W*3
+  const int64_t pitch8 = 3LL * W * (kThreads / 32);
+  const uint8_t* src_row = frame + ((int64_t)(y0 - R + warp) * W + x) * 3;
   auto load_row = [&](int v, uint4& a, uint4& b, uint4& d) {
     const int y = y0 - R + v;
     if (v < G::ROWS && y >= 0 && y < H && col_ok) {
-      const uint8_t* src = frame + ((int64_t)y * W + x) * 3;
-      a = ldg_nc_v4(src);
-      b = ldg_nc_v4(src + 16);
-      d = ldg_nc_v4(src + 32);
+      a = ldg_nc_v4(src_row);
+      b = ldg_nc_v4(src_row + 16);
+      d = ldg_nc_v4(src_row + 32);
     } else {
       a = b = d = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
     }
+    src_row += pitch8;
   };
   uint4 na, nb, nd;
   load_row(warp, na, nb, nd);
@@ -178,13 +184,23 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
     vert_levels<L, N>(hi);
     uint32_t mx = 0;
     if (xo < W) {
-      uint8_t* dst = dark + (int64_t)f * dark_fs + (int64_t)(y0 + j0) * W + xo;
+      uint32_t* dst = reinterpret_cast<uint32_t*>(dark + (int64_t)f * dark_fs + (int64_t)(y0 + j0) * W + xo);
+      const int wstep = W >> 2;  // row pitch in words (W % 16 == 0 on this path)
+      if (y0 + j0 + kRun <= H) {  // whole run inside the frame: no per-row checks
 #pragma unroll
-      for (int j = 0; j < kRun; ++j) {
-        const uint32_t a = vert_final<L, N>(lo, j), b = vert_final<L, N>(hi, j);
-        if (y0 + j0 + j < H) {
-          *reinterpret_cast<uint32_t*>(dst + (int64_t)j * W) = pack2(a, b);
+        for (int j = 0; j < kRun; ++j) {
+          const uint32_t a = vert_final<L, N>(lo, j), b = vert_final<L, N>(hi, j);
+          dst[j * wstep] = pack2(a, b);
           mx = max3u(mx, a, b);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kRun; ++j) {
+          const uint32_t a = vert_final<L, N>(lo, j), b = vert_final<L, N>(hi, j);
+          if (y0 + j0 + j < H) {
+            dst[j * wstep] = pack2(a, b);
+            mx = max3u(mx, a, b);
+          }
         }
       }
     }
