@@ -38,6 +38,7 @@ constexpr int kT1 = 256;            // R1 threads
 constexpr int kT2 = 1024;           // R2 threads
 constexpr int kCap = 4096;          // R2 candidates kept in shared memory
 constexpr int kT3 = 256;            // R3 threads
+constexpr int kColTab = 2048;       // R3: output widths up to this use a column-tap table
 
 __device__ __forceinline__ double u8f(uint32_t v) { return __ddiv_rn((double)v, 255.0); }
 
@@ -57,14 +58,28 @@ __device__ __forceinline__ Tap tap(int i, double scale, int n) {
   return t;
 }
 
-// Resized RGB at output (y, x): rows blend first, then columns, clip (imageops.py:74-78).
-__device__ __forceinline__ void resized_rgb(const uint8_t* __restrict__ frame, const ResizeGeo& G, int y, int x,
-                                            const double* __restrict__ s_f, double (&rgb)[3]) {
-  const Tap ty = tap(y, G.sy, G.h), tx = tap(x, G.sx, G.w);
-  const uint8_t* p00 = frame + ((int64_t)ty.i0 * G.w + tx.i0) * 3;
-  const uint8_t* p01 = frame + ((int64_t)ty.i0 * G.w + tx.i1) * 3;
-  const uint8_t* p10 = frame + ((int64_t)ty.i1 * G.w + tx.i0) * 3;
-  const uint8_t* p11 = frame + ((int64_t)ty.i1 * G.w + tx.i1) * 3;
+// Compact column/row tap for shared-memory tables: i1 = min(i0 + 1, n - 1) and
+// g = 1 - f are recomputed (one op each) from (i0, f).
+struct TapS {
+  int i0;
+  double f;
+};
+__device__ __forceinline__ Tap expand(const TapS& c, int n) {
+  Tap t;
+  t.i0 = c.i0;
+  t.i1 = min(c.i0 + 1, n - 1);
+  t.f = c.f;
+  t.g = __dsub_rn(1.0, c.f);
+  return t;
+}
+__device__ __forceinline__ TapS compact(const Tap& t) { return TapS{t.i0, t.f}; }
+
+// Resized RGB from its row and column taps: rows blend first, then columns, clip
+// (imageops.py:74-78).  Every term is >= 0, so the clip reduces to min(., 1).
+__device__ __forceinline__ void resized_rgb_t(const uint8_t* __restrict__ frame, int w, const Tap& ty,
+                                              const Tap& tx, const double* __restrict__ s_f, double (&rgb)[3]) {
+  const uint8_t* p00 = frame + ((int64_t)ty.i0 * w + tx.i0) * 3;
+  const uint8_t* p10 = frame + ((int64_t)ty.i1 * w + tx.i0) * 3;
   // A zero weight makes a blend exact: RN(RN(a*1) + RN(b*0)) == a for a >= 0 (integer
   // scale factors, e.g. 1920 -> 640, hit this on every column), so that tap is skipped.
   if (tx.f == 0.0) {
@@ -74,16 +89,23 @@ __device__ __forceinline__ void resized_rgb(const uint8_t* __restrict__ frame, c
     } else {
 #pragma unroll
       for (int c = 0; c < 3; ++c)
-        rgb[c] = fmin(fmax(__dadd_rn(__dmul_rn(s_f[p00[c]], ty.g), __dmul_rn(s_f[p10[c]], ty.f)), 0.0), 1.0);
+        rgb[c] = fmin(__dadd_rn(__dmul_rn(s_f[p00[c]], ty.g), __dmul_rn(s_f[p10[c]], ty.f)), 1.0);
     }
     return;
   }
+  const uint8_t* p01 = frame + ((int64_t)ty.i0 * w + tx.i1) * 3;
+  const uint8_t* p11 = frame + ((int64_t)ty.i1 * w + tx.i1) * 3;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const double r0 = __dadd_rn(__dmul_rn(s_f[p00[c]], ty.g), __dmul_rn(s_f[p10[c]], ty.f));
     const double r1 = __dadd_rn(__dmul_rn(s_f[p01[c]], ty.g), __dmul_rn(s_f[p11[c]], ty.f));
-    rgb[c] = fmin(fmax(__dadd_rn(__dmul_rn(r0, tx.g), __dmul_rn(r1, tx.f)), 0.0), 1.0);
+    rgb[c] = fmin(__dadd_rn(__dmul_rn(r0, tx.g), __dmul_rn(r1, tx.f)), 1.0);
   }
+}
+
+__device__ __forceinline__ void resized_rgb(const uint8_t* __restrict__ frame, const ResizeGeo& G, int y, int x,
+                                            const double* __restrict__ s_f, double (&rgb)[3]) {
+  resized_rgb_t(frame, G.w, tap(y, G.sy, G.h), tap(x, G.sx, G.w), s_f, rgb);
 }
 
 __device__ __forceinline__ int bucket_of(double d) { return min(max((int)(d * 4096.0), 0), kResizeBuckets - 1); }
@@ -123,15 +145,19 @@ k_rs_dark_t(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, double* 
   const int ty0 = blockIdx.y * kTH, tx0 = blockIdx.x * kTW;
   double* cm = sm;              // [PH][PW] resized channel minimum (clamped coordinates)
   double* rm = sm + PH * PW;    // [PH][kTW] row minima
+  __shared__ TapS s_ty[PH], s_tx[PW];
   s_f[threadIdx.x] = u8f(threadIdx.x);
   for (int b = threadIdx.x; b < kResizeBuckets; b += kT1) s_hist[b] = 0;
+  for (int k = threadIdx.x; k < PH + PW; k += kT1) {
+    if (k < PH) s_ty[k] = compact(tap(min(max(ty0 - R + k, 0), G.H - 1), G.sy, G.h));
+    else s_tx[k - PH] = compact(tap(min(max(tx0 - R + k - PH, 0), G.W - 1), G.sx, G.w));
+  }
   __syncthreads();
   const uint8_t* frame = in + (int64_t)f * in_fs;
   for (int e = threadIdx.x; e < PH * PW; e += kT1) {
     const int py = e / PW, px = e - py * PW;
-    const int y = min(max(ty0 - R + py, 0), G.H - 1), x = min(max(tx0 - R + px, 0), G.W - 1);
     double rgb[3];
-    resized_rgb(frame, G, y, x, s_f, rgb);
+    resized_rgb_t(frame, G.w, expand(s_ty[py], G.h), expand(s_tx[px], G.w), s_f, rgb);
     cm[e] = fmin(fmin(rgb[0], rgb[1]), rgb[2]);  // estimation.py:38
   }
   __syncthreads();
@@ -468,6 +494,7 @@ k_rs_recover(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const d
   __shared__ double s_f[256];
   __shared__ double s_thr[MODE == 2 ? 3 : 1][256];
   __shared__ double red[3][kT3 / 32];
+  __shared__ TapS s_tx[kColTab];
   const int f = blockIdx.y;
   s_f[threadIdx.x] = u8f(threadIdx.x);
   if (MODE == 0) s_thr[0][threadIdx.x] = thr[threadIdx.x];
@@ -476,6 +503,7 @@ k_rs_recover(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const d
   __syncthreads();
   const double A0 = airlight[3 * f], A1 = airlight[3 * f + 1], A2 = airlight[3 * f + 2];
   const double amax = fmax(fmax(A0, A1), A2);
+  const double ramax = __drcp_rn(amax);  // cmin / amax as the exact div_rb
   const float ig = (float)inv_gamma;
   float g0 = 1.0f, g1 = 1.0f, g2 = 1.0f;
   if (MODE == 2) {
@@ -485,14 +513,19 @@ k_rs_recover(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const d
   }
   const uint8_t* frame = in + (int64_t)f * in_fs;
   uint8_t* fo = out + (int64_t)f * out_fs;
-  const int64_t npx = (int64_t)G.H * G.W;
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-  for (int64_t p = (int64_t)blockIdx.x * kT3 + threadIdx.x; p < npx; p += (int64_t)gridDim.x * kT3) {
-    const int y = (int)(p / G.W), x = (int)(p - (int64_t)y * G.W);
+  // rows [r0, r1) of the output; column taps tabulated once per CTA
+  const int r0 = (int)((int64_t)G.H * blockIdx.x / gridDim.x), r1 = (int)((int64_t)G.H * (blockIdx.x + 1) / gridDim.x);
+  const bool tab = G.W <= kColTab;
+  for (int x = threadIdx.x; tab && x < G.W; x += kT3) s_tx[x] = compact(tap(x, G.sx, G.w));
+  __syncthreads();
+  for (int y = r0; y < r1; ++y)
+  for (int x = threadIdx.x; x < G.W; x += kT3) {
+    const int64_t p = (int64_t)y * G.W + x;
     double rgb[3];
-    resized_rgb(frame, G, y, x, s_f, rgb);
+    resized_rgb_t(frame, G.w, tap(y, G.sy, G.h), tab ? expand(s_tx[x], G.w) : tap(x, G.sx, G.w), s_f, rgb);
     const double cmin = fmin(fmin(rgb[0], rgb[1]), rgb[2]);
-    const double t = fmin(fmax(__dsub_rn(1.0, __dmul_rn(omega, __ddiv_rn(cmin, amax))), t_min), 1.0);
+    const double t = fmin(fmax(__dsub_rn(1.0, __dmul_rn(omega, div_rb(cmin, amax, ramax))), t_min), 1.0);
     const double rt = __drcp_rn(t);
     const double x0 = recover_x(rgb[0], A0, t, rt), x1 = recover_x(rgb[1], A1, t, rt),
                  x2 = recover_x(rgb[2], A2, t, rt);
@@ -594,7 +627,7 @@ cudaError_t resize_recover(const uint8_t* in, int64_t in_fs, int n, const Resize
   const int g1 = gamma == 1.0 ? 1 : 0;
   if (!balance) {
     const int64_t want = std::max<int64_t>(1, (8LL * sm_count() + n - 1) / std::max(n, 1));
-    const int bx = (int)std::max<int64_t>(1, std::min<int64_t>((npx + kT3 - 1) / kT3, want));
+    const int bx = (int)std::max<int64_t>(1, std::min<int64_t>(g.H, want));  // row blocks per frame
     k_rs_recover<0><<<dim3(bx, n), kT3, 0, st>>>(in, in_fs, g, airlight, omega, t_min, thr, nullptr, ig, g1, out,
                                                  out_fs, nullptr);
     return cudaGetLastError();
