@@ -83,7 +83,7 @@ __device__ __forceinline__ uint32_t vert_final(const uint32_t (&v)[N], int j) {
 }
 
 template <int R>
-__global__ void __launch_bounds__(kThreads, DHZ_K1_MINB)
+__global__ void __launch_bounds__(kThreads, R <= 8 ? DHZ_K1_MINB : 1)
 k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t* __restrict__ dark,
             int64_t dark_fs, uint32_t* __restrict__ frame_max, uint32_t* __restrict__ blk_max) {
   using G = RowGeo<R>;

@@ -104,7 +104,7 @@ __device__ __forceinline__ void thread_offsets(double (&tot)[NQ], double (*wt)[k
 // ---------------------------------------------------------------- pass 1 ----
 // a, b for every pixel of the strip x in [x0, x0 + 256*CPT - 2r), rows [y0, y0 + seg).
 template <int CPT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, CPT == 4 ? 3 : 4)
 k_gf_pass1(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, int seg, double eps,
            const double* __restrict__ airlight, double omega, double t_min, double* __restrict__ a_out,
            double* __restrict__ b_out) {
