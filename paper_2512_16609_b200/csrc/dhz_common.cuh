@@ -221,36 +221,49 @@ __device__ __forceinline__ double div_rb(double a, double b, double rb) {
   return __fma_rn(r, rb, q);
 }
 
-// x^e for x in [0, 1], e > 0, to a few ulp (exp(e*log(x)) with a 2*atanh
-// series for the log and a degree-13 Taylor exp) — used only inside the
-// gray-world channel sums, where per-sample errors of ~1e-16 are far below the
-// reference's own summation rounding.  Bytes are never derived from it.
-__device__ __forceinline__ double pow_unit(double x, double e) {
+// x^e for x in [0, 1], e > 0, used only inside the gray-world channel sums, where
+// per-sample errors of a few ulp (absolute < 4e-16 on [0.01, 1]) are far below the
+// reference's own summation rounding; bytes are never derived from it.  Table
+// driven (tables per CTA in shared memory): ln(x) = ex*ln2 + ln(c_j) +
+// ln(1 + eps) with c_j the centre of x's 1/128-mantissa interval (|eps| < 2^-8,
+// degree-7 series), exp(y) = 2^(k/64) * exp(r) with |r| <= ln2/128 (degree 6).
+struct PowTables {
+  double lnc[128];   // ln(c_j), c_j = 1 + (j + 0.5) / 128
+  double rinv[128];  // RN(1 / c_j)
+  double e2[64];     // 2^(j / 64)
+};
+
+__device__ __forceinline__ void pow_tables_init(PowTables& T) {
+  for (int j = threadIdx.x; j < 128; j += blockDim.x) {
+    const double c = 1.0 + ((double)j + 0.5) / 128.0;
+    T.lnc[j] = log(c);
+    T.rinv[j] = __ddiv_rn(1.0, c);
+    if (j < 64) T.e2[j] = exp2((double)j / 64.0);
+  }
+}
+
+__device__ __forceinline__ double pow_tab(double x, double e, const PowTables& T) {
   if (!(x >= 0x1p-1000)) return 0.0;  // (recovered values are 0 or far above this)
   if (x >= 1.0) return 1.0;
   const long long bits = __double_as_longlong(x);
-  int ex = (int)(bits >> 52) - 1022;                                           // x = m * 2^ex
-  double m = __longlong_as_double((bits & 0x000fffffffffffffLL) | 0x3fe0000000000000LL);  // m in [0.5, 1)
-  if (m < 0.70710678118654752) { m = m * 2.0; ex -= 1; }   // m in [sqrt(1/2), sqrt(2))
-  const double s = (m - 1.0) * __drcp_rn(m + 1.0);
-  const double s2 = s * s;
-  double p = 1.0 / 23;
-  p = fma(p, s2, 1.0 / 21); p = fma(p, s2, 1.0 / 19); p = fma(p, s2, 1.0 / 17); p = fma(p, s2, 1.0 / 15);
-  p = fma(p, s2, 1.0 / 13); p = fma(p, s2, 1.0 / 11); p = fma(p, s2, 1.0 / 9);  p = fma(p, s2, 1.0 / 7);
-  p = fma(p, s2, 1.0 / 5);  p = fma(p, s2, 1.0 / 3);
-  const double lnm = 2.0 * fma(p * s2, s, s);  // 2 atanh(s) = ln(m)
+  const int ex = (int)(bits >> 52) - 1023;                                   // x = m * 2^ex, m in [1, 2)
+  const int j = (int)((bits >> 45) & 127);
+  const double m = __longlong_as_double((bits & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
+  const double eps = fma(m, T.rinv[j], -1.0);
+  double p = 1.0 / 7;
+  p = fma(p, eps, -1.0 / 6); p = fma(p, eps, 1.0 / 5); p = fma(p, eps, -1.0 / 4);
+  p = fma(p, eps, 1.0 / 3);  p = fma(p, eps, -0.5);    p = fma(p, eps, 1.0);
   constexpr double kLn2Hi = 6.93147180369123816490e-01, kLn2Lo = 1.90821492927058770002e-10;
-  const double y = e * fma((double)ex, kLn2Hi, fma((double)ex, kLn2Lo, lnm));   // e * ln(x) <= 0
-  if (y < -700.0) return 0.0;  // keeps 2^k normal below
-  const double k = rint(y * 1.44269504088896340736);
-  const double r = fma(-k, kLn2Lo, fma(-k, kLn2Hi, y));  // |r| <= ~0.35
-  double q = 1.0 / 6227020800.0;                          // 1/13!
-  q = fma(q, r, 1.0 / 479001600.0); q = fma(q, r, 1.0 / 39916800.0); q = fma(q, r, 1.0 / 3628800.0);
-  q = fma(q, r, 1.0 / 362880.0);    q = fma(q, r, 1.0 / 40320.0);    q = fma(q, r, 1.0 / 5040.0);
-  q = fma(q, r, 1.0 / 720.0);       q = fma(q, r, 1.0 / 120.0);      q = fma(q, r, 1.0 / 24.0);
-  q = fma(q, r, 1.0 / 6.0);         q = fma(q, r, 0.5);              q = fma(q, r, 1.0);
-  q = fma(q, r, 1.0);
-  return q * __longlong_as_double((long long)((int)k + 1023) << 52);  // k in [-1010, 0]
+  const double y = e * fma((double)ex, kLn2Hi, fma((double)ex, kLn2Lo, T.lnc[j] + p * eps));  // e ln x <= 0
+  if (y < -700.0) return 0.0;
+  constexpr double kL64Hi = 0x1.62e42fefa0000p-7, kL64Lo = 2.572804622327669e-14;  // ln2/64 = hi + lo
+  const double k = rint(y * 92.332482616893656);                                     // 64 / ln2
+  const double r = fma(-k, kL64Lo, fma(-k, kL64Hi, y));
+  double q = 1.0 / 720;
+  q = fma(q, r, 1.0 / 120); q = fma(q, r, 1.0 / 24); q = fma(q, r, 1.0 / 6);
+  q = fma(q, r, 0.5);       q = fma(q, r, 1.0);      q = fma(q, r, 1.0);
+  const int ki = (int)k;
+  return q * T.e2[ki & 63] * __longlong_as_double((long long)((ki >> 6) + 1023) << 52);
 }
 
 // clip(((v/255 - A) / t) + A, 0, 1) with the division done as div_rb(., t, RN(1/t)).

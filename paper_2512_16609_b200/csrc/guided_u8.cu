@@ -224,6 +224,7 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
   constexpr int NC = kThreads * CPT;
   __shared__ GuideTables T;  // wr/wg/wb for the guide; t[] holds v/255 here
   __shared__ double sA[3], s_thr[256];
+  __shared__ PowTables PT;  // balance sums (MODE 1)
   extern __shared__ double dyn_pre[];  // [2 buffers][2 sums][NC + 1] prefix rows
   __shared__ double wt[2][2][kThreads / 32];
   auto pre = [&](int buf, int q) { return dyn_pre + (buf * 2 + q) * (NC + 1); };
@@ -241,6 +242,7 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
   }
   if (threadIdx.x < 3) sA[threadIdx.x] = airlight[3 * f + threadIdx.x];
   if (threadIdx.x < 4) pre(threadIdx.x >> 1, threadIdx.x & 1)[0] = 0.0;
+  if (MODE == 1) pow_tables_init(PT);
   __syncthreads();
   int xc[CPT];
 #pragma unroll
@@ -319,9 +321,9 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
             acc1 = __dadd_rn(acc1, x1v);
             acc2 = __dadd_rn(acc2, x2v);
           } else {
-            acc0 = __dadd_rn(acc0, pow_unit(x0v, inv_gamma));
-            acc1 = __dadd_rn(acc1, pow_unit(x1v, inv_gamma));
-            acc2 = __dadd_rn(acc2, pow_unit(x2v, inv_gamma));
+            acc0 = __dadd_rn(acc0, pow_tab(x0v, inv_gamma, PT));
+            acc1 = __dadd_rn(acc1, pow_tab(x1v, inv_gamma, PT));
+            acc2 = __dadd_rn(acc2, pow_tab(x2v, inv_gamma, PT));
           }
         }
       }

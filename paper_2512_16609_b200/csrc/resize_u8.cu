@@ -495,8 +495,10 @@ k_rs_recover(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const d
   __shared__ double s_thr[MODE == 2 ? 3 : 1][256];
   __shared__ double red[3][kT3 / 32];
   __shared__ TapS s_tx[kColTab];
+  __shared__ PowTables PT;  // balance sums (MODE 1)
   const int f = blockIdx.y;
   s_f[threadIdx.x] = u8f(threadIdx.x);
+  if (MODE == 1) pow_tables_init(PT);
   if (MODE == 0) s_thr[0][threadIdx.x] = thr[threadIdx.x];
   if (MODE == 2)
     for (int c = 0; c < 3; ++c) s_thr[c][threadIdx.x] = thr[((int64_t)f * 3 + c) * 256 + threadIdx.x];
@@ -535,9 +537,9 @@ k_rs_recover(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const d
         acc1 = __dadd_rn(acc1, x1);
         acc2 = __dadd_rn(acc2, x2);
       } else {
-        acc0 = __dadd_rn(acc0, pow_unit(x0, inv_gamma));
-        acc1 = __dadd_rn(acc1, pow_unit(x1, inv_gamma));
-        acc2 = __dadd_rn(acc2, pow_unit(x2, inv_gamma));
+        acc0 = __dadd_rn(acc0, pow_tab(x0, inv_gamma, PT));
+        acc1 = __dadd_rn(acc1, pow_tab(x1, inv_gamma, PT));
+        acc2 = __dadd_rn(acc2, pow_tab(x2, inv_gamma, PT));
       }
     } else {
       const double* t0 = s_thr[0];
