@@ -266,6 +266,13 @@ __device__ __forceinline__ double pow_tab(double x, double e, const PowTables& T
   return q * T.e2[ki & 63] * __longlong_as_double((long long)((ki >> 6) + 1023) << 52);
 }
 
+// ((x - A) / t) + A without the final clip: where the value only feeds the byte
+// thresholds (x < 0 -> byte 0, x > 1 -> the byte of 1) or pow_tab (0 / 1 outside
+// (0, 1)), clipping first gives the same result, so the clip is skipped there.
+__device__ __forceinline__ double recover_raw(double x, double A, double t, double rt) {
+  return __dadd_rn(div_rb(__dsub_rn(x, A), t, rt), A);
+}
+
 // clip(((v/255 - A) / t) + A, 0, 1) with the division done as div_rb(., t, RN(1/t)).
 __device__ __forceinline__ double recover_x(double x, double A, double t, double rt) {
   return fmin(fmax(__dadd_rn(div_rb(__dsub_rn(x, A), t, rt), A), 0.0), 1.0);

@@ -306,8 +306,8 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
         double t = fmin(fmax(__dadd_rn(__dmul_rn(ma, g), mb), 0.0), 1.0);
         t = fmax(t, t_min);  // pipeline.py:203
         const double rt = __drcp_rn(t);
-        const double x0v = recover_x(T.t[R], A0, t, rt), x1v = recover_x(T.t[G], A1, t, rt),
-                     x2v = recover_x(T.t[B], A2, t, rt);
+        const double x0v = recover_raw(T.t[R], A0, t, rt), x1v = recover_raw(T.t[G], A1, t, rt),
+                     x2v = recover_raw(T.t[B], A2, t, rt);
         if (MODE == 0) {
           uint8_t* o = out + (int64_t)f * out_fs + pix * 3;
           const float ig = (float)inv_gamma;
@@ -317,9 +317,9 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
         } else {
           t_out[fo + pix] = t;
           if (gamma_is_one) {
-            acc0 = __dadd_rn(acc0, x0v);
-            acc1 = __dadd_rn(acc1, x1v);
-            acc2 = __dadd_rn(acc2, x2v);
+            acc0 = __dadd_rn(acc0, fmin(fmax(x0v, 0.0), 1.0));
+            acc1 = __dadd_rn(acc1, fmin(fmax(x1v, 0.0), 1.0));
+            acc2 = __dadd_rn(acc2, fmin(fmax(x2v, 0.0), 1.0));
           } else {
             acc0 = __dadd_rn(acc0, pow_tab(x0v, inv_gamma, PT));
             acc1 = __dadd_rn(acc1, pow_tab(x1v, inv_gamma, PT));
@@ -444,7 +444,7 @@ k_gf_apply(const uint8_t* __restrict__ in, int64_t in_fs, int64_t npx, const dou
         for (int c = 0; c < 3; ++c) {
           const double Ac = c == 0 ? A0 : (c == 1 ? A1 : A2);
           const float gc = c == 0 ? gn0 : (c == 1 ? gn1 : gn2);
-          const double x = recover_x(s_f[v[u][c]], Ac, t[u], rt);
+          const double x = recover_raw(s_f[v[u][c]], Ac, t[u], rt);
           fo[3 * p + c] = (uint8_t)quantize_thr_from(x, s_thr[c], guess_byte(x, ig, gc));
         }
       }

@@ -529,13 +529,13 @@ k_rs_recover(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const d
     const double cmin = fmin(fmin(rgb[0], rgb[1]), rgb[2]);
     const double t = fmin(fmax(__dsub_rn(1.0, __dmul_rn(omega, div_rb(cmin, amax, ramax))), t_min), 1.0);
     const double rt = __drcp_rn(t);
-    const double x0 = recover_x(rgb[0], A0, t, rt), x1 = recover_x(rgb[1], A1, t, rt),
-                 x2 = recover_x(rgb[2], A2, t, rt);
+    const double x0 = recover_raw(rgb[0], A0, t, rt), x1 = recover_raw(rgb[1], A1, t, rt),
+                 x2 = recover_raw(rgb[2], A2, t, rt);
     if (MODE == 1) {
       if (gamma_is_one) {
-        acc0 = __dadd_rn(acc0, x0);
-        acc1 = __dadd_rn(acc1, x1);
-        acc2 = __dadd_rn(acc2, x2);
+        acc0 = __dadd_rn(acc0, fmin(fmax(x0, 0.0), 1.0));
+        acc1 = __dadd_rn(acc1, fmin(fmax(x1, 0.0), 1.0));
+        acc2 = __dadd_rn(acc2, fmin(fmax(x2, 0.0), 1.0));
       } else {
         acc0 = __dadd_rn(acc0, pow_tab(x0, inv_gamma, PT));
         acc1 = __dadd_rn(acc1, pow_tab(x1, inv_gamma, PT));
