@@ -47,8 +47,9 @@ __device__ __forceinline__ void load_guide(GuideTables& T, int v, double x) {
   T.wb[v] = __dmul_rn(0.114, x);
 }
 
+// (the guide's weighted sum of non-negative terms is >= 0: its clip reduces to min(., 1))
 __device__ __forceinline__ double guide_t(const GuideTables& T, uint32_t r, uint32_t g, uint32_t b) {
-  return fmin(fmax(__dadd_rn(__dadd_rn(T.wr[r], T.wg[g]), T.wb[b]), 0.0), 1.0);
+  return fmin(__dadd_rn(__dadd_rn(T.wr[r], T.wg[g]), T.wb[b]), 1.0);
 }
 
 // The same guide value without table lookups (shared-memory traffic binds pass 1):
@@ -58,7 +59,7 @@ __device__ __forceinline__ double guide_arith(uint32_t r, uint32_t g, uint32_t b
   constexpr double rk = 0x1.0101010101010p-8;  // RN(1/255)
   const double xr = div_rb((double)r, k255, rk), xg = div_rb((double)g, k255, rk), xb = div_rb((double)b, k255, rk);
   const double v = __dadd_rn(__dadd_rn(__dmul_rn(0.299, xr), __dmul_rn(0.587, xg)), __dmul_rn(0.114, xb));
-  return fmin(fmax(v, 0.0), 1.0);
+  return fmin(v, 1.0);  // v >= 0
 }
 
 // tot[q] (this thread's sum over its columns) -> the CTA-exclusive prefix before
@@ -303,8 +304,8 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
         const uint8_t* px = frame + pix * 3;
         const uint32_t R = px[0], G = px[1], B = px[2];
         const double g = guide_t(T, R, G, B);
-        double t = fmin(fmax(__dadd_rn(__dmul_rn(ma, g), mb), 0.0), 1.0);
-        t = fmax(t, t_min);  // pipeline.py:203
+        // clip(q, 0, 1) then max(., t_min) (estimation.py:172, pipeline.py:203) == clip(q, t_min, 1)
+        const double t = fmin(fmax(__dadd_rn(__dmul_rn(ma, g), mb), t_min), 1.0);
         const double rt = __drcp_rn(t);
         const double x0v = recover_raw(T.t[R], A0, t, rt), x1v = recover_raw(T.t[G], A1, t, rt),
                      x2v = recover_raw(T.t[B], A2, t, rt);
