@@ -57,6 +57,50 @@ class TestValidation:
             check_radius(-1)
 
 
+class TestRouting:
+    """Which calls the batched native pipelines cover (pipeline._native_ok) — the rest
+    run the per-frame float64 device path; no device is needed to decide."""
+
+    def test_video(self):
+        from paper_2512_16609_b200.pipeline import RESIZE_MAX_RADIUS, _native_ok
+
+        assert _native_ok(DehazeParams(resize_to=None), 1080, 1920)
+        assert _native_ok(DehazeParams(), 480, 640)                   # resize is a no-op
+        assert _native_ok(DehazeParams(), 1080, 1920)                 # default resize path
+        assert not _native_ok(DehazeParams(), 1080, 1920, want_maps=True)
+        assert _native_ok(DehazeParams(resize_to=None), 1080, 1920, want_maps=True)
+        assert _native_ok(DehazeParams(patch_radius=RESIZE_MAX_RADIUS), 100, 100)
+        assert not _native_ok(DehazeParams(patch_radius=RESIZE_MAX_RADIUS + 1), 100, 100)
+        assert _native_ok(DehazeParams(resize_to=None, patch_radius=60), 100, 100)
+
+    def test_image(self):
+        from paper_2512_16609_b200.pipeline import GUIDED_MAX_RADIUS, _native_ok
+
+        img = DehazeParams.for_image()
+        assert _native_ok(img, 1080, 1920)
+        assert not _native_ok(img, 1080, 1920, want_maps=True)
+        assert _native_ok(DehazeParams.for_image(guided_radius=GUIDED_MAX_RADIUS), 64, 64)
+        assert not _native_ok(DehazeParams.for_image(guided_radius=GUIDED_MAX_RADIUS + 1), 64, 64)
+        assert not _native_ok(DehazeParams.for_image(resize_to=(320, 240)), 1080, 1920)
+
+    def test_working_size(self):
+        from paper_2512_16609_b200.engine import FrameEngine
+
+        assert FrameEngine.working_size(DehazeParams(), 1080, 1920) == (480, 640)
+        assert FrameEngine.working_size(DehazeParams(resize_to=None), 1080, 1920) == (1080, 1920)
+        assert FrameEngine.working_size(DehazeParams(resize_to=(33, 7)), 50, 60) == (7, 33)
+
+    def test_guided_limits_match_the_library(self):
+        # the Python routing constants mirror the C++ ones (dhz_internal.h)
+        import re
+
+        from paper_2512_16609_b200 import pipeline
+
+        src = open(os.path.join(os.path.dirname(pipeline.__file__), "csrc", "dhz_internal.h")).read()
+        assert int(re.search(r"kGuidedMaxRadius = (\d+)", src).group(1)) == pipeline.GUIDED_MAX_RADIUS
+        assert int(re.search(r"kResizeMaxRadius = (\d+)", src).group(1)) == pipeline.RESIZE_MAX_RADIUS
+
+
 class TestSharding:
     @pytest.mark.parametrize("n,world", [(300, 1), (300, 2), (300, 8), (7, 3), (2, 4), (0, 2)])
     def test_shard_range_partitions(self, n, world):
