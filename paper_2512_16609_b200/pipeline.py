@@ -395,8 +395,95 @@ def dehaze_host_batch(frames, params=None, out=None, airlight=None, chunk=None):
     return out, airlight
 
 
-_STREAM_BATCH_BYTES = 256 << 20   # ~256 MiB of input frames per device launch
+_STREAM_BATCH_BYTES = 256 << 20   # float path: ~256 MiB of input frames per device launch
 _STREAM_BATCH_MAX = 256
+_PIPE_BATCH_BYTES = 48 << 20      # native path: input bytes per pipelined batch
+_PIPE_SLOTS = 3
+
+
+class _StreamPipe:
+    """process_stream's pipelined batches on the native path.
+
+    Each slot owns pinned host staging (input, output, airlight), device buffers,
+    a stream and an engine.  Frames are copied into a slot's pinned input as they
+    arrive; a full slot is submitted (H2D, fused pipeline, D2H, all async on its
+    stream) and the host goes on filling the next slot, so PCIe transfers and
+    kernels of batch k overlap the host copies of batch k+1.  Slots are drained
+    (outputs handed to the sink) in submission order, which keeps frame order.
+    """
+
+    def __init__(self, dev, params, shape):
+        import torch
+
+        from .engine import FrameEngine
+
+        H, W, _ = shape
+        OH, OW = FrameEngine.working_size(params, H, W)
+        self.batch = max(1, min(_STREAM_BATCH_MAX, _PIPE_BATCH_BYTES // (3 * H * W)))
+        self.params = params
+        self.out_shape = (OH, OW, 3)
+        S, B = _PIPE_SLOTS, self.batch
+        pin = dict(dtype=torch.uint8, pin_memory=True)
+        self.hin = [torch.empty((B, H, W, 3), **pin) for _ in range(S)]
+        self.hout = [torch.empty((B, OH, OW, 3), **pin) for _ in range(S)]
+        self.hair = [torch.empty((B, 3), dtype=torch.float64, pin_memory=True) for _ in range(S)]
+        self.din = [torch.empty((B, H, W, 3), dtype=torch.uint8, device=dev) for _ in range(S)]
+        self.dout = [torch.empty((B, OH, OW, 3), dtype=torch.uint8, device=dev) for _ in range(S)]
+        self.dair = [torch.empty((B, 3), dtype=torch.float64, device=dev) for _ in range(S)]
+        self.streams = [torch.cuda.Stream(dev) for _ in range(S)]
+        self.engines = [FrameEngine(dev) for _ in range(S)]
+        self.events = [torch.cuda.Event() for _ in range(S)]
+        self.inflight = [0] * S
+        self.slot = 0
+        self.fill = 0
+
+    def put(self, frame, emit):
+        import torch
+
+        s = self.slot
+        if self.fill == 0 and self.inflight[s]:
+            self.drain(s, emit)
+        self.hin[s][self.fill].copy_(torch.from_numpy(frame))
+        self.fill += 1
+        if self.fill == self.batch:
+            self.submit()
+
+    def submit(self):
+        import torch
+
+        s, m = self.slot, self.fill
+        if m == 0:
+            return
+        st = self.streams[s]
+        with torch.cuda.stream(st):
+            self.din[s][:m].copy_(self.hin[s][:m], non_blocking=True)
+            self.engines[s].run(self.din[s][:m], self.params, out=self.dout[s][:m], airlight=self.dair[s][:m],
+                                stream=st)
+            self.hout[s][:m].copy_(self.dout[s][:m], non_blocking=True)
+            self.hair[s][:m].copy_(self.dair[s][:m], non_blocking=True)
+            self.events[s].record(st)
+        self.inflight[s] = m
+        self.slot = (s + 1) % len(self.hin)
+        self.fill = 0
+
+    def drain(self, s, emit):
+        import torch
+
+        m = self.inflight[s]
+        if not m:
+            return
+        self.events[s].synchronize()
+        for i in range(m):
+            out = np.empty(self.out_shape, dtype=np.uint8)   # the sink may keep it: a fresh array
+            torch.from_numpy(out).copy_(self.hout[s][i])
+            emit(out, self.hair[s][i].numpy().copy())
+        self.inflight[s] = 0
+
+    def finish(self, emit):
+        self.submit()
+        S = len(self.hin)
+        for k in range(S):  # oldest first: the slot after the last submitted one
+            self.drain((self.slot + k) % S, emit)
 
 
 def process_stream(frames, params=None, sink=None, workers=1):
@@ -405,6 +492,8 @@ def process_stream(frames, params=None, sink=None, workers=1):
     Frames are validated as they arrive and dehazed in device batches; each
     output frame reaches ``sink`` in input order.  A mid-stream size change
     raises after every frame before it has been dehazed and handed to the sink.
+    On the native paths the batches are pipelined (``_StreamPipe``); ``workers``
+    keeps the reference's contract (>= 1; results never depend on it).
     """
     if params is None:
         params = DehazeParams()
@@ -419,9 +508,19 @@ def process_stream(frames, params=None, sink=None, workers=1):
     start = time.perf_counter()
     pending = []
     dev = None
+    pipe = None
+
+    def emit(out, air):
+        nonlocal count
+        if sink is not None:
+            sink(out)
+        trace.append(air)
+        count += 1
 
     def flush():
-        nonlocal count
+        if pipe is not None:
+            pipe.finish(emit)
+            return
         if not pending:
             return
         batch = _as_device_batch(np.stack(pending), dev)
@@ -429,10 +528,7 @@ def process_stream(frames, params=None, sink=None, workers=1):
         out_h = out.cpu().numpy()
         air_h = air.cpu().numpy()
         for i in range(len(pending)):
-            if sink is not None:
-                sink(out_h[i])
-            trace.append(air_h[i].copy())
-            count += 1
+            emit(out_h[i], air_h[i].copy())
         pending.clear()
 
     for index, frame in enumerate(frames):
@@ -445,6 +541,8 @@ def process_stream(frames, params=None, sink=None, workers=1):
                 dev = _device()
                 per = frame.nbytes
                 limit = max(1, min(_STREAM_BATCH_MAX, _STREAM_BATCH_BYTES // max(per, 1)))
+                if _native_ok(params, frame.shape[0], frame.shape[1]):
+                    pipe = _StreamPipe(dev, params, frame.shape)
             elif frame.shape != expected_shape:
                 raise ValueError(
                     f"frame {index} has size {frame.shape[1]}x{frame.shape[0]}, "
@@ -453,6 +551,9 @@ def process_stream(frames, params=None, sink=None, workers=1):
         except ValueError:
             flush()
             raise
+        if pipe is not None:
+            pipe.put(frame, emit)
+            continue
         pending.append(frame)
         if len(pending) >= limit:
             flush()
