@@ -167,6 +167,8 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
 
   // ---------------- pass 2: vertical min, thread per 4 columns x 16 rows ----------------
   constexpr int NG = kTW / 4;                 // 120 column groups
+  // the warp shuffles below need whole warps in every iteration of the item loop
+  static_assert((NG * (kBH / kRun)) % 32 == 0, "pass-2 items must fill whole warps");
   constexpr int N = kRun + 2 * R;
   uint32_t tmax = 0;
   for (int it = threadIdx.x; it < NG * (kBH / kRun); it += kThreads) {
