@@ -34,6 +34,18 @@ namespace {
 inline int cuda_fail(cudaError_t e, const char* where) { return dhz::abi_cuda_fail(e, where); }
 
 constexpr int64_t kAlign = 256;
+
+// Stage events: inside a CUDA-graph capture they become event-record nodes
+// (external records), so a replayed graph still timestamps every stage.
+void record_stage_event(void* const* events, int i, cudaStream_t st) {
+  if (!events || !events[i]) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(reinterpret_cast<cudaEvent_t>(events[i]), st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[i]), st);
+}
 int64_t align_up(int64_t v, int64_t a = kAlign) { return (v + a - 1) / a * a; }
 
 struct Layout {
@@ -144,9 +156,7 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const d
     return fail(DHZ_E_UNSUPPORTED, "patch_radius %d too large for the tiled erosion", p->patch_radius);
 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  auto mark = [&](int i) {
-    if (events && events[i]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[i]), st);
-  };
+  auto mark = [&](int i) { record_stage_event(events, i, st); };
   mark(0);
   uint8_t* base = static_cast<uint8_t*>(ws);
   cudaError_t e = cudaMemsetAsync(base, 0, (size_t)L.zero_end, st);  // maxima, select state, histograms
@@ -277,9 +287,7 @@ int dhz_frames_resize_u8(const uint8_t* in, int64_t in_fs, int n, int h, int w, 
   if (!ws || (int64_t)ws_bytes < L.total)
     return fail(DHZ_E_WORKSPACE, "workspace too small: need %lld bytes, got %zu", (long long)L.total, ws_bytes);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  auto mark = [&](int i) {
-    if (events && events[i]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[i]), st);
-  };
+  auto mark = [&](int i) { record_stage_event(events, i, st); };
   const dhz::ResizeGeo g = make_geo(h, w, H, W);
   uint8_t* base = static_cast<uint8_t*>(ws);
   double* dark = reinterpret_cast<double*>(base + L.dark);

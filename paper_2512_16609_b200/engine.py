@@ -184,10 +184,12 @@ class GraphedPipeline:
     overlaps another chunk's LUT pass (shared-memory bound) and the recovery pass
     finds its chunk's frames in L2; the graph removes the per-launch host cost
     that would otherwise dominate small chunks.  Inputs/outputs are the tensors
-    given at construction (update ``frames`` in place between replays).
+    given at construction (update ``frames`` in place between replays).  With
+    ``streams == 1``, ``events`` (DHZ_N_EVENTS timing events) are recorded by every
+    replay at the stage boundaries.
     """
 
-    def __init__(self, frames, params, out=None, airlight=None, streams=2, chunk=8):
+    def __init__(self, frames, params, out=None, airlight=None, streams=2, chunk=8, events=None):
         self.frames = frames
         self.params = params
         self.out = out if out is not None else torch.empty_like(frames)
@@ -201,12 +203,15 @@ class GraphedPipeline:
             run = lambda: self._eng.run(self.frames, params, out=self.out, airlight=self.airlight, chunk=chunk)  # noqa: E731
         else:
             self._eng = FrameEngine(frames.device)
-            run = lambda: self._eng.run(self.frames, params, out=self.out, airlight=self.airlight)  # noqa: E731
+            run = lambda ev=None: self._eng.run(self.frames, params, out=self.out, airlight=self.airlight,  # noqa: E731
+                                                events=ev)
         run()  # eager warm-up: workspaces, thresholds, kernel attributes
         torch.cuda.synchronize(frames.device)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            run()
+            # stage events (single-stream only) are captured as event-record nodes:
+            # every replay re-timestamps them
+            run(events) if streams == 1 and events is not None else run()
         torch.cuda.synchronize(frames.device)
 
     def replay(self):
