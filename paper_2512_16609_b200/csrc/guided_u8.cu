@@ -453,20 +453,14 @@ k_gf_apply(const uint8_t* __restrict__ in, int64_t in_fs, int64_t npx, const dou
   }
 }
 
-// Columns per thread: the widest strip (4, 2 or 1 columns per thread, i.e.
-// 1024/512/256 input columns) that still leaves >= 2 CTAs per SM; wider strips
-// waste fewer halo columns and amortise the per-row prefix over more columns.
-int guided_cpt(int H, int W, int r, int n) {
-  for (int cpt = 4; cpt >= 1; cpt >>= 1) {
-    const int sw = cpt * kThreads - 2 * r;
-    if (sw < 1) return cpt * 2;
-    const int64_t ctas = (int64_t)((W + sw - 1) / sw) * n * ((H + 15) / 16);
-    if (ctas >= 2 * 148 || cpt == 1) {
-      if (2 * r >= cpt * kThreads) return cpt * 2;
-      return cpt;
-    }
-  }
-  return 1;
+// Columns per thread (strip width 256*CPT input columns) from the frame width and
+// radius only — never from the batch size, so a frame's box-sum rounding (and its
+// bytes) do not depend on which batch it came in.  Wider strips waste fewer halo
+// columns and amortise the per-row prefix; narrow frames keep more CTAs.
+int guided_cpt(int W, int r) {
+  int cpt = W >= 4096 ? 4 : (W >= 1024 ? 2 : 1);
+  while (2 * r >= cpt * kThreads) cpt *= 2;  // the strip must hold the window
+  return cpt;
 }
 
 template <int CPT>
@@ -480,15 +474,16 @@ cudaError_t balance_thresholds(const double* part, int nparts, int n, int64_t np
   return cudaGetLastError();
 }
 
-// Rows per CTA segment: long segments amortise the 2r+1-row warm-up of the
-// sliding sums, short ones give small batches enough CTAs.
-int guided_seg_rows(int H, int W, int r, int n, int cpt) {
+// Rows per CTA segment, again from the frame geometry only: about 2 CTAs per SM for
+// one frame; long enough (>= 16 rows and >= r) that the 2r+1-row warm-up of the
+// sliding sums stays cheap next to the segment's own rows.
+int guided_seg_rows(int H, int W, int r, int cpt) {
   const int sw = kThreads * cpt - 2 * r;
-  const int64_t strips = (int64_t)((W + sw - 1) / sw) * n;
-  const int64_t want = 6 * 148;
+  const int64_t strips = (W + sw - 1) / sw;
+  const int64_t want = 2 * 148;
   int64_t segs = std::max<int64_t>(1, (want + strips - 1) / strips);
   int seg = (int)((H + segs - 1) / segs);
-  seg = std::max(seg, std::min(H, std::max(16, r)));  // the 2r+1-row warm-up is cheap next to a row
+  seg = std::max(seg, std::min(H, std::max(16, r)));
   return std::min(seg, 1024);
 }
 
@@ -503,13 +498,9 @@ size_t guided_ws_bytes(int n, int H, int W, int r, bool balance) {
   const int c = guided_chunk(n, H, W, balance);
   size_t b = 16ull * npx * c;                                            // a, b
   if (balance) {
-    int64_t parts = 0;
-    for (int cpt = 1; cpt <= 4; cpt <<= 1) {  // any strip width may be chosen for the chunk
-      const int sw = kThreads * cpt - 2 * r;
-      if (sw < 1) continue;
-      const int seg = guided_seg_rows(H, W, r, c, cpt);
-      parts = std::max<int64_t>(parts, (int64_t)((W + sw - 1) / sw) * ((H + seg - 1) / seg));
-    }
+    const int cpt = guided_cpt(W, r), sw = kThreads * cpt - 2 * r;
+    const int seg = guided_seg_rows(H, W, r, cpt);
+    const int64_t parts = (int64_t)((W + sw - 1) / sw) * ((H + seg - 1) / seg);
     b += 8ull * npx * c + 24ull * parts * c + 3 * 256 * 8ull * c + 16ull * c;  // t~, sums, thresholds, gains
   }
   return b;
@@ -525,9 +516,9 @@ cudaError_t guided_recover_u8(const uint8_t* in, int64_t in_fs, int n, int H, in
   const int g1 = gamma == 1.0 ? 1 : 0;
   for (int f0 = 0; f0 < n; f0 += chunk) {
     const int c = std::min(chunk, n - f0);
-    const int cpt = guided_cpt(H, W, r, c);
+    const int cpt = guided_cpt(W, r);
     const int sw = kThreads * cpt - 2 * r;
-    const int seg = guided_seg_rows(H, W, r, c, cpt);
+    const int seg = guided_seg_rows(H, W, r, cpt);
     dim3 grid((W + sw - 1) / sw, (H + seg - 1) / seg, c);
     const uint8_t* fin = in + (int64_t)f0 * in_fs;
     uint8_t* fout = out + (int64_t)f0 * out_fs;
