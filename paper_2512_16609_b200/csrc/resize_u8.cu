@@ -133,46 +133,69 @@ __device__ __forceinline__ void window_min(const double (&v)[S + 2 * R], double 
 
 // Tile kernel with the erosion radius fixed at compile time (register windows).
 template <int R>
-__global__ void __launch_bounds__(kT1)
+__global__ void __launch_bounds__(kT1, R <= 7 ? 4 : 2)
 k_rs_dark_t(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, double* __restrict__ dark,
             uint32_t* __restrict__ hist) {
   constexpr int S = 8;                       // outputs per thread and pass
   constexpr int PH = kTH + 2 * R, PW = kTW + 2 * R;
+  constexpr int kRowItems = PH * (kTW / S);
+  constexpr int kRowIter = (kRowItems + kT1 - 1) / kT1;
+  constexpr int kHistWords = (kResizeBuckets + 1) / 2;  // 16-bit counters (a tile has <= 2048 outputs)
   extern __shared__ double sm[];
   __shared__ double s_f[256];
-  __shared__ uint32_t s_hist[kResizeBuckets];
+  __shared__ uint32_t s_hist[kHistWords];
   const int f = blockIdx.z;
   const int ty0 = blockIdx.y * kTH, tx0 = blockIdx.x * kTW;
-  double* cm = sm;              // [PH][PW] resized channel minimum (clamped coordinates)
-  double* rm = sm + PH * PW;    // [PH][kTW] row minima
+  double* cm = sm;  // [PH][PW] resized channel minimum (clamped coordinates); then [PH][kTW] row minima
   __shared__ TapS s_ty[PH], s_tx[PW];
   s_f[threadIdx.x] = u8f(threadIdx.x);
-  for (int b = threadIdx.x; b < kResizeBuckets; b += kT1) s_hist[b] = 0;
+  for (int b = threadIdx.x; b < kHistWords; b += kT1) s_hist[b] = 0;
   for (int k = threadIdx.x; k < PH + PW; k += kT1) {
     if (k < PH) s_ty[k] = compact(tap(min(max(ty0 - R + k, 0), G.H - 1), G.sy, G.h));
     else s_tx[k - PH] = compact(tap(min(max(tx0 - R + k - PH, 0), G.W - 1), G.sx, G.w));
   }
   __syncthreads();
   const uint8_t* frame = in + (int64_t)f * in_fs;
-  for (int e = threadIdx.x; e < PH * PW; e += kT1) {
-    const int py = e / PW, px = e - py * PW;
-    double rgb[3];
+  // two samples per iteration: both samples' byte loads are in flight together
+  for (int e = threadIdx.x; e < PH * PW; e += 2 * kT1) {
+    const int e2 = min(e + kT1, PH * PW - 1);
+    const int py = e / PW, px = e - py * PW, py2 = e2 / PW, px2 = e2 - py2 * PW;
+    double rgb[3], rgb2[3];
     resized_rgb_t(frame, G.w, expand(s_ty[py], G.h), expand(s_tx[px], G.w), s_f, rgb);
+    resized_rgb_t(frame, G.w, expand(s_ty[py2], G.h), expand(s_tx[px2], G.w), s_f, rgb2);
     cm[e] = fmin(fmin(rgb[0], rgb[1]), rgb[2]);  // estimation.py:38
+    if (e + kT1 < PH * PW) cm[e2] = fmin(fmin(rgb2[0], rgb2[1]), rgb2[2]);
   }
   __syncthreads();
-  // rows first (morphology.py:73): item = (row, 8-column segment)
-  for (int e = threadIdx.x; e < PH * (kTW / S); e += kT1) {
-    const int py = e / (kTW / S), seg = e - py * (kTW / S);
-    const double* row = cm + py * PW + seg * S;
-    double v[S + 2 * R], o[S];
+  // rows first (morphology.py:73): item = (row, 8-column segment); all of a thread's
+  // windows are reduced into registers before the row minima overwrite cm in place
+  {
+    double o[kRowIter][S];
 #pragma unroll
-    for (int i = 0; i < S + 2 * R; ++i) v[i] = row[i];
-    window_min<R, S>(v, o);
+    for (int k = 0; k < kRowIter; ++k) {
+      const int e = threadIdx.x + k * kT1;
+      if (e < kRowItems) {
+        const int py = e / (kTW / S), seg = e - py * (kTW / S);
+        const double* row = cm + py * PW + seg * S;
+        double v[S + 2 * R];
 #pragma unroll
-    for (int i = 0; i < S; ++i) rm[py * kTW + seg * S + i] = o[i];
+        for (int i = 0; i < S + 2 * R; ++i) v[i] = row[i];
+        window_min<R, S>(v, o[k]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kRowIter; ++k) {
+      const int e = threadIdx.x + k * kT1;
+      if (e < kRowItems) {
+        const int py = e / (kTW / S), seg = e - py * (kTW / S);
+#pragma unroll
+        for (int i = 0; i < S; ++i) cm[py * kTW + seg * S + i] = o[k][i];
+      }
+    }
   }
   __syncthreads();
+  const double* rm = cm;  // [PH][kTW]
   // columns: item = (column, 8-row segment); lanes take consecutive columns
   const int64_t npx = (int64_t)G.H * G.W;
   for (int e = threadIdx.x; e < kTW * (kTH / S); e += kT1) {
@@ -188,13 +211,17 @@ k_rs_dark_t(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, double* 
       const int y = ty0 + seg * S + i;
       if (y < G.H && x < G.W) {
         dark[(int64_t)f * npx + (int64_t)y * G.W + x] = o[i];
-        atomicAdd(&s_hist[bucket_of(o[i])], 1u);
+        const int b = bucket_of(o[i]);
+        atomicAdd(&s_hist[b >> 1], 1u << (16 * (b & 1)));
       }
     }
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < kResizeBuckets; b += kT1)
-    if (s_hist[b]) atomicAdd(&hist[(int64_t)f * kResizeBuckets + b], s_hist[b]);
+  for (int w = threadIdx.x; w < kHistWords; w += kT1) {
+    const uint32_t c2 = s_hist[w];
+    if (c2 & 0xFFFFu) atomicAdd(&hist[(int64_t)f * kResizeBuckets + 2 * w], c2 & 0xFFFFu);
+    if (c2 >> 16) atomicAdd(&hist[(int64_t)f * kResizeBuckets + 2 * w + 1], c2 >> 16);
+  }
 }
 
 // Generic radius (runtime r, loops over the window in shared memory).
@@ -581,11 +608,12 @@ cudaError_t resize_dark(const uint8_t* in, int64_t in_fs, int n, const ResizeGeo
                         uint32_t* hist, cudaStream_t st) {
   if (r < 1 || r > kResizeMaxRadius) return cudaErrorInvalidValue;
   const size_t smem = (size_t)((kTH + 2 * r) * (kTW + 2 * r) + (kTH + 2 * r) * kTW) * sizeof(double);
+  const size_t smem_t = (size_t)(kTH + 2 * r) * (kTW + 2 * r) * sizeof(double);  // row minima in place
   dim3 grid((g.W + kTW - 1) / kTW, (g.H + kTH - 1) / kTH, n);
   auto launch = [&](auto kern) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kT1, smem, st>>>(in, in_fs, g, dark, hist);
+    kern<<<grid, kT1, smem_t, st>>>(in, in_fs, g, dark, hist);
     return cudaGetLastError();
   };
   switch (r) {
