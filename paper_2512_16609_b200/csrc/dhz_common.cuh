@@ -273,9 +273,5 @@ __device__ __forceinline__ double recover_raw(double x, double A, double t, doub
   return __dadd_rn(div_rb(__dsub_rn(x, A), t, rt), A);
 }
 
-// clip(((v/255 - A) / t) + A, 0, 1) with the division done as div_rb(., t, RN(1/t)).
-__device__ __forceinline__ double recover_x(double x, double A, double t, double rt) {
-  return fmin(fmax(__dadd_rn(div_rb(__dsub_rn(x, A), t, rt), A), 0.0), 1.0);
-}
 
 }  // namespace dhz

@@ -125,3 +125,18 @@ def test_balance_degenerate_black(oracle):
     out, air, _, _ = _run(frames, p)
     for i, f in enumerate(frames):
         assert np.array_equal(out[i], oracle.dehaze_frame(f, p))
+
+
+@pytest.mark.parametrize("shape", [(37, 53), (24, 30)])
+def test_balance_odd_shapes_scalar_path(oracle, shape):
+    # widths that are not a multiple of 16 take the scalar balance-sum and K6 kernels
+    rng = np.random.default_rng(29)
+    frames = rng.integers(0, 256, size=(2,) + shape + (3,), dtype=np.uint8)
+    p = _params(white_balance=True)
+    out, air, _, _ = _run(frames, p)
+    for i, f in enumerate(frames):
+        m = {}
+        want = oracle.dehaze_frame(f, p, m)
+        assert np.array_equal(air[i], m["airlight"])
+        d = np.abs(out[i].astype(np.int16) - want.astype(np.int16))
+        assert d.max() <= 1 and int((d > 0).sum()) <= 2
