@@ -373,7 +373,10 @@ def dehaze_host_batch(frames, params=None, out=None, airlight=None, chunk=None):
         return out, airlight
     if chunk is None:
         chunk = max(1, min(n, (48 << 20) // (3 * H * W)))
-    key = (dev.index, chunk, H, W, OH, OW)
+    import threading
+
+    # per thread, like engine_for: concurrent callers never share staging buffers
+    key = (dev.index, threading.get_ident(), chunk, H, W, OH, OW)
     pipe = _host_pipes.get(key)
     if pipe is None:
         pipe = _host_pipes[key] = _HostPipe(dev, chunk, H, W, OH, OW)
