@@ -34,6 +34,7 @@ namespace {
 inline int cuda_fail(cudaError_t e, const char* where) { return dhz::abi_cuda_fail(e, where); }
 
 constexpr int64_t kAlign = 256;
+constexpr int kMaxFrames = 65535;  // frames ride grid.y / grid.z
 
 // Stage events: inside a CUDA-graph capture they become event-record nodes
 // (external records), so a replayed graph still timestamps every stage.
@@ -90,6 +91,7 @@ Layout make_layout(int n, int H, int W, const dhz_params* p) {
 int check_params(int n, int H, int W, const dhz_params* p) {
   if (!p) return fail(DHZ_E_INVALID, "params is NULL");
   if (n < 0) return fail(DHZ_E_INVALID, "n_frames must be >= 0, got %d", n);
+  if (n > kMaxFrames) return fail(DHZ_E_INVALID, "n_frames %d above %d per call (grid limit): split the batch", n, kMaxFrames);
   if (H < 1 || W < 1) return fail(DHZ_E_INVALID, "empty frame %dx%d", W, H);
   const int64_t npx = (int64_t)H * W;
   if (npx > 0xFFFFFFF0LL) return fail(DHZ_E_INVALID, "frame too large (%lld px)", (long long)npx);

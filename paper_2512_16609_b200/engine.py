@@ -18,6 +18,9 @@ from . import _native
 from .quant import device_thresholds
 
 
+MAX_FRAMES_PER_CALL = 65535  # abi.cu kMaxFrames (frames ride grid.y / grid.z)
+
+
 def top_k(npx: int, top_fraction: float) -> int:
     """estimation.py:72 — K = max(1, floor(top_fraction * n)), Python float arithmetic."""
     return max(1, math.floor(top_fraction * npx))
@@ -96,6 +99,11 @@ class FrameEngine:
             airlight = torch.empty((n, 3), dtype=torch.float64, device=dev)
         if n == 0:
             return (out, airlight, {}) if keep_maps else (out, airlight)
+        if n > MAX_FRAMES_PER_CALL and not keep_maps:  # the library takes <= 65535 frames per call
+            for lo in range(0, n, MAX_FRAMES_PER_CALL):
+                hi = min(n, lo + MAX_FRAMES_PER_CALL)
+                self.run(frames[lo:hi], params, out=out[lo:hi], airlight=airlight[lo:hi], stream=stream)
+            return out, airlight
         st = stream if stream is not None else torch.cuda.current_stream(dev)
         ev_arr = None
         if events is not None:

@@ -33,3 +33,19 @@ def test_abi_version_and_errors():
     p.top_k, p.patch_radius, p.thresholds = 5, 1, None
     assert lib.dhz_frames_u8_workspace(1, 4, 4, ctypes.byref(p)) == 0
     assert b"thresholds" in lib.dhz_last_error()
+
+
+def test_batch_limit_rejected_without_a_device():
+    import ctypes
+
+    from paper_2512_16609_b200 import _native
+    from paper_2512_16609_b200.engine import MAX_FRAMES_PER_CALL
+
+    lib = _native.load_library()
+    p = _native.DhzParams()
+    p.mode, p.patch_radius, p.top_k, p.guided_radius = 0, 7, 1, 40
+    p.alpha, p.omega, p.t_min, p.guided_eps, p.gamma = 0.8, 0.5, 0.05, 1e-3, 1.2
+    p.thresholds = 1  # any non-NULL pointer: only the argument checks run
+    assert lib.dhz_frames_u8_workspace(MAX_FRAMES_PER_CALL, 4, 4, ctypes.byref(p)) > 0
+    assert lib.dhz_frames_u8_workspace(MAX_FRAMES_PER_CALL + 1, 4, 4, ctypes.byref(p)) == 0
+    assert b"split the batch" in lib.dhz_last_error()

@@ -140,3 +140,19 @@ def test_balance_odd_shapes_scalar_path(oracle, shape):
         assert np.array_equal(air[i], m["airlight"])
         d = np.abs(out[i].astype(np.int16) - want.astype(np.int16))
         assert d.max() <= 1 and int((d > 0).sum()) <= 2
+
+
+def test_batches_beyond_the_grid_limit(oracle):
+    # more frames than one launch takes (65535): the engine splits the batch
+    from paper_2512_16609_b200 import dehaze_batch
+
+    rng = np.random.default_rng(31)
+    n = 70000
+    frames = rng.integers(0, 256, size=(n, 2, 3, 3), dtype=np.uint8)
+    p = _params()
+    out, air = dehaze_batch(torch.from_numpy(frames).cuda(), p)
+    out, air = out.cpu().numpy(), air.cpu().numpy()
+    for i in (0, 65534, 65535, n - 1):
+        m = {}
+        want = oracle.dehaze_frame(frames[i], p, m)
+        assert np.array_equal(out[i], want) and np.array_equal(air[i], m["airlight"])
