@@ -415,7 +415,7 @@ class _StreamPipe:
     (outputs handed to the sink) in submission order, which keeps frame order.
     """
 
-    def __init__(self, dev, params, shape):
+    def __init__(self, dev, params, shape, fresh=True):
         import torch
 
         from .engine import FrameEngine
@@ -439,17 +439,27 @@ class _StreamPipe:
         self.inflight = [0] * S
         self.slot = 0
         self.fill = 0
+        self.fresh = fresh  # False: emit views of the pinned output (the consumer copies at once)
+        self._emit = None
+
+    def next_input(self, emit=None):
+        """The pinned input frame the next frame goes into (drains the slot's previous batch first)."""
+        s = self.slot
+        if self.fill == 0 and self.inflight[s]:
+            self.drain(s, emit if emit is not None else self._emit)
+        return self.hin[s][self.fill]
+
+    def commit(self, emit):
+        self._emit = emit
+        self.fill += 1
+        if self.fill == self.batch:
+            self.submit()
 
     def put(self, frame, emit):
         import torch
 
-        s = self.slot
-        if self.fill == 0 and self.inflight[s]:
-            self.drain(s, emit)
-        self.hin[s][self.fill].copy_(torch.from_numpy(frame))
-        self.fill += 1
-        if self.fill == self.batch:
-            self.submit()
+        self.next_input(emit).copy_(torch.from_numpy(frame))
+        self.commit(emit)
 
     def submit(self):
         import torch
@@ -477,8 +487,11 @@ class _StreamPipe:
             return
         self.events[s].synchronize()
         for i in range(m):
-            out = np.empty(self.out_shape, dtype=np.uint8)   # the sink may keep it: a fresh array
-            torch.from_numpy(out).copy_(self.hout[s][i])
+            if self.fresh:
+                out = np.empty(self.out_shape, dtype=np.uint8)   # the sink may keep it: a fresh array
+                torch.from_numpy(out).copy_(self.hout[s][i])
+            else:
+                out = self.hout[s][i].numpy()
             emit(out, self.hair[s][i].numpy().copy())
         self.inflight[s] = 0
 
@@ -534,7 +547,17 @@ def process_stream(frames, params=None, sink=None, workers=1):
             emit(out_h[i], air_h[i].copy())
         pending.clear()
 
-    for index, frame in enumerate(frames):
+    it = iter(frames)
+    index = -1
+    while True:
+        index += 1
+        try:
+            frame = next(it)
+        except StopIteration:
+            break
+        except BaseException:
+            flush()  # frames before a failing source (e.g. a truncated stream) still reach the sink
+            raise
         try:
             frame = check_u8_frame(frame, name=f"frame {index}")
             if not isinstance(frame, np.ndarray):

@@ -29,3 +29,22 @@ for name, p in (("native", DehazeParams(resize_to=None)), ("default-resize", Deh
     dehaze_host_batch(pin, p)
     el = time.perf_counter() - t0
     print(f"dehaze_host_batch {name}: {n / el:.0f} fps ({el * 1e3:.1f} ms)")
+
+# raw RGB24 streams: reader + process_stream + writer vs the pinned-staging path
+import io
+
+from paper_2512_16609_b200.frameio import StreamHeader, dehaze_raw_stream, read_raw_frames, write_raw_frame
+
+raw = b"".join(f.tobytes() for f in frames)
+hdr = StreamHeader(width=1920, height=1080)
+for name, p in (("native", DehazeParams(resize_to=None)), ("default-resize", DehazeParams())):
+    dst = io.BytesIO()
+    t0 = time.perf_counter()
+    process_stream(read_raw_frames(io.BytesIO(raw), hdr), p, sink=lambda f: write_raw_frame(dst, f))
+    el = time.perf_counter() - t0
+    dst2 = io.BytesIO()
+    t0 = time.perf_counter()
+    dehaze_raw_stream(io.BytesIO(raw), dst2, hdr, p)
+    el2 = time.perf_counter() - t0
+    print(f"raw stream {name}: reader+process_stream+writer {n / el:.0f} fps, dehaze_raw_stream {n / el2:.0f} fps,"
+          f" same bytes {dst.getvalue() == dst2.getvalue()}")
