@@ -475,15 +475,15 @@ cudaError_t balance_thresholds(const double* part, int nparts, int n, int64_t np
 }
 
 // Rows per CTA segment, again from the frame geometry only: about 2 CTAs per SM for
-// one frame; long enough (>= 16 rows and >= r) that the 2r+1-row warm-up of the
-// sliding sums stays cheap next to the segment's own rows.
+// one frame; at least 16 rows (a shorter floor tied to r cost single images more
+// parallelism than the 2r+1-row warm-up of the sliding sums saves).
 int guided_seg_rows(int H, int W, int r, int cpt) {
   const int sw = kThreads * cpt - 2 * r;
   const int64_t strips = (W + sw - 1) / sw;
   const int64_t want = 2 * 148;
   int64_t segs = std::max<int64_t>(1, (want + strips - 1) / strips);
   int seg = (int)((H + segs - 1) / segs);
-  seg = std::max(seg, std::min(H, std::max(16, r)));
+  seg = std::max(seg, std::min(H, 16));
   return std::min(seg, 1024);
 }
 
