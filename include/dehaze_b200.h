@@ -15,6 +15,8 @@
  *    row-major, maps are (H, W) row-major.
  *  - The library never allocates device memory: callers pass a workspace sized by
  *    the matching *_workspace() query.
+ *  - A batch call takes at most 65535 frames (DHZ_E_INVALID otherwise; split larger
+ *    batches).  A frame's output never depends on the batch it arrives in.
  *  - Return value 0 = success; negative = error, message in dhz_last_error()
  *    (thread-local).  Argument validation with the reference's ValueError messages
  *    stays on the host side (paper_2512_16609_b200/validation.py); the C side only
