@@ -17,10 +17,10 @@ import torch
 from . import _native
 from .quant import device_thresholds
 from .validation import (
-    RANGE_SLACK,
     check_float_image_shape,
     check_same_shape,
     check_scalar_map_shape,
+    check_stats,
 )
 
 F64 = torch.float64
@@ -70,10 +70,7 @@ def check_float_image(x, name="image", clip=False):
     t = to_device_f64(x)
     check_float_image_shape(tuple(t.shape), name)
     ok, lo, hi = stats(t)
-    if not ok:
-        raise ValueError(f"{name}: contains non-finite samples")
-    if not clip and (lo < -RANGE_SLACK or hi > 1.0 + RANGE_SLACK):
-        raise ValueError(f"{name}: samples outside [0, 1] (min {lo:.6g}, max {hi:.6g})")
+    check_stats(name, ok, lo, hi, clip)
     if lo < 0.0 or hi > 1.0:
         t = t.clamp(0.0, 1.0)
     return t
@@ -84,8 +81,7 @@ def check_scalar_map(x, name="map"):
     t = to_device_f64(x)
     check_scalar_map_shape(tuple(t.shape), name)
     ok, lo, hi = stats(t)
-    if not ok:
-        raise ValueError(f"{name}: contains non-finite samples")
+    check_stats(name, ok, lo, hi, clip=True)  # maps: finiteness only
     return t
 
 
