@@ -1,0 +1,66 @@
+"""Randomised parity sweep: random frame sizes and DehazeParams (both modes, resize
+on/off, balance on/off, extreme top_fraction / gamma / omega / t_min) through the
+batched native paths against the CPU oracle.  Seeded; each case is small so the
+oracle stays fast.  Same bars as the targeted tests: airlight bit-exact, output
+<= 1 LSB with at most 2 differing samples per frame (0 expected without the guided
+filter or balance)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(rng):
+    from paper_2512_16609_b200 import DehazeParams
+
+    mode = "image" if rng.random() < 0.35 else "video"
+    h, w = int(rng.integers(1, 90)), int(rng.integers(1, 120))
+    resize = None
+    if mode == "video" and rng.random() < 0.4:
+        resize = (int(rng.integers(1, 100)), int(rng.integers(1, 80)))
+    p = DehazeParams(
+        mode=mode,
+        patch_radius=int(rng.choice([1, 2, 3, 5, 7, 11, 16])),
+        top_fraction=float(rng.choice([0.001, 0.01, 0.1, 0.5, 1.0])),
+        alpha=float(rng.uniform(0.3, 1.0)),
+        omega=float(rng.uniform(0.2, 1.0)),
+        t_min=float(rng.choice([0.01, 0.05, 0.2, 0.5])),
+        guided_radius=int(rng.choice([1, 2, 4, 8, 20, 60])),
+        guided_eps=float(rng.choice([1e-4, 1e-3, 1e-2])),
+        gamma=float(rng.choice([1.0, 1.2, 0.7, 2.2])),
+        white_balance=bool(rng.random() < 0.5),
+        resize_to=resize,
+    )
+    n = int(rng.integers(1, 4))
+    kind = rng.integers(0, 3)
+    if kind == 0:
+        frames = rng.integers(0, 256, size=(n, h, w, 3), dtype=np.uint8)
+    elif kind == 1:  # hazy-ish: bright, low contrast
+        frames = np.clip(rng.normal(190, 20, size=(n, h, w, 3)), 0, 255).astype(np.uint8)
+    else:  # flat patches (ties everywhere)
+        frames = np.repeat(rng.integers(0, 256, size=(n, 1, 1, 3), dtype=np.uint8), h, 1).repeat(w, 2)
+    return p, np.ascontiguousarray(frames)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_cases(oracle, seed):
+    from paper_2512_16609_b200 import dehaze_batch
+    from paper_2512_16609_b200.pipeline import _native_ok
+
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(6):
+        p, frames = _case(rng)
+        assert _native_ok(p, frames.shape[1], frames.shape[2]) or p.mode == "image"
+        out, air = dehaze_batch(torch.from_numpy(frames).cuda(), p)
+        out, air = out.cpu().numpy(), air.cpu().numpy()
+        exact = p.mode == "video" and not p.balance_enabled()
+        for i, f in enumerate(frames):
+            m = {}
+            want = oracle.dehaze_frame(f, p, m)
+            assert out[i].shape == want.shape, (p, f.shape)
+            assert np.array_equal(air[i], m["airlight"]), (p, f.shape, air[i], m["airlight"])
+            d = np.abs(out[i].astype(np.int16) - want.astype(np.int16))
+            assert d.max() <= 1, (p, f.shape, int(d.max()))
+            assert int((d > 0).sum()) <= (0 if exact else 2), (p, f.shape, int((d > 0).sum()))
