@@ -64,3 +64,25 @@ def test_random_cases(oracle, seed):
             d = np.abs(out[i].astype(np.int16) - want.astype(np.int16))
             assert d.max() <= 1, (p, f.shape, int(d.max()))
             assert int((d > 0).sum()) <= (0 if exact else 2), (p, f.shape, int((d > 0).sum()))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_cases_aligned_widths(oracle, seed):
+    # widths that are multiples of 16 take the vectorised fast paths (K1 rows, K6 with
+    # the diagonal split, banded balance sums); larger frames reach the wide guided strips
+    from paper_2512_16609_b200 import dehaze_batch
+
+    rng = np.random.default_rng(5000 + seed)
+    for _ in range(4):
+        p, _ = _case(rng)
+        h, w = int(rng.integers(8, 400)), 16 * int(rng.integers(1, 80))
+        frames = np.clip(rng.normal(170, 40, size=(2, h, w, 3)), 0, 255).astype(np.uint8)
+        out, air = dehaze_batch(torch.from_numpy(frames).cuda(), p)
+        out, air = out.cpu().numpy(), air.cpu().numpy()
+        exact = p.mode == "video" and not p.balance_enabled()
+        for i, f in enumerate(frames):
+            m = {}
+            want = oracle.dehaze_frame(f, p, m)
+            assert np.array_equal(air[i], m["airlight"]), (p, f.shape)
+            d = np.abs(out[i].astype(np.int16) - want.astype(np.int16))
+            assert d.max() <= 1 and int((d > 0).sum()) <= (0 if exact else 2), (p, f.shape, int((d > 0).sum()))
