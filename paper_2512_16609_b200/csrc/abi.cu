@@ -51,7 +51,7 @@ int64_t align_up(int64_t v, int64_t a = kAlign) { return (v + a - 1) / a * a; }
 
 struct Layout {
   // [0, zero_end) is cleared at the start of every call
-  int64_t frame_max, sel, blk_max, row_hist, frame_hist, zero_end;
+  int64_t frame_max, sel, blk_max, row_hist, frame_hist, hist256, zero_end;
   int64_t row_info, sel_idx, lut, bal, dark, tmap, total;
   int64_t dark_fs;
 };
@@ -72,6 +72,7 @@ Layout make_layout(int n, int H, int W, const dhz_params* p) {
   L.blk_max = take(4LL * n * nb * ntx);
   L.row_hist = take(4LL * dhz::kWin * n * H);
   L.frame_hist = take(4LL * dhz::kWin * n);
+  L.hist256 = take(4LL * 256 * n);
   L.zero_end = o;
   L.row_info = take(16LL * n * H);
   L.sel_idx = take(4LL * n * std::max<int64_t>(1, p->top_k));
@@ -177,6 +178,7 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const d
   sw.blk_max = bmax;
   sw.row_hist = reinterpret_cast<uint32_t*>(base + L.row_hist);
   sw.frame_hist = reinterpret_cast<uint32_t*>(base + L.frame_hist);
+  sw.hist256 = reinterpret_cast<uint32_t*>(base + L.hist256);
   sw.row_info = reinterpret_cast<uint32_t*>(base + L.row_info);
   sw.sel_idx = reinterpret_cast<uint32_t*>(base + L.sel_idx);
   sw.H = H;

@@ -40,6 +40,7 @@ struct SelectWs {
   uint32_t* blk_max;     // [n][ceil(H/16)][ceil(W/480)] max dark value per block (K1 output)
   uint32_t* row_hist;    // [n][H][16] pixels per row at level max-j, zeroed by the caller
   uint32_t* frame_hist;  // [n][16], zeroed by the caller
+  uint32_t* hist256;     // [n][256] full level histogram (fallback frames only), zeroed by the caller
   uint32_t* row_info;    // [n][H][4] = above, ties, above_prefix, tie_prefix
   uint32_t* sel_idx;     // [n][K] selected flat indices in summation order
   int H, W;

@@ -18,7 +18,8 @@
 // K3 (k_threshold): CTA per frame: T = K-th largest level, per-row (above,
 //   tie) counts and their exclusive prefixes over rows (linear index order).
 //   Frames whose top K spans more than 16 levels are redone by K3b
-//   (k_threshold_full, full 256-level histogram; an early exit otherwise).
+//   (k_full_hist/_threshold/_rows/_scan: a full 256-level histogram and per-row
+//   counts spread over many CTAs per frame; frames on the fast path exit at once).
 // K4 (k_compact_sum): CTA per frame: warps compact the few rows that hold
 //   selected pixels (ballot-free: per-lane counts + warp scan, index order),
 //   then the gather and the three sequential fp64 channel sums.
@@ -178,38 +179,75 @@ k_threshold(int64_t npx, int64_t K, int H, const uint32_t* __restrict__ frame_ma
   });
 }
 
-// Fallback: the top K pixels span more than kWin levels below the max.
+// Fallback for frames whose top K spans more than kWin levels below the max
+// (sel.mode == kSelFull): a full 256-level histogram and per-row counts, each
+// spread over kFullParts CTAs per frame (frames on the fast path exit at once).
+constexpr int kFullParts = 32;
+
+// F1: 256-level histogram of the frame's dark bytes (warp-private shared copies).
 template <bool VEC>
 __global__ void __launch_bounds__(kT)
-k_threshold_full(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_t K, int H, int W,
-                 FrameSel* __restrict__ sel, uint32_t* __restrict__ row_info) {
-  const int f = blockIdx.x;
+k_full_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, const FrameSel* __restrict__ sel,
+            uint32_t* __restrict__ hist256) {
+  const int f = blockIdx.y, part = blockIdx.x;
   if (sel[f].mode != kSelFull) return;
+  __shared__ uint32_t h[kWarps][256];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < kWarps * 256; k += kT) (&h[0][0])[k] = 0;
+  __syncthreads();
   const uint8_t* p = dark + f * dark_fs;
-  __shared__ uint32_t h[256];
-  __shared__ uint32_t T_s;
-  h[threadIdx.x] = 0;
-  __syncthreads();
-  for (int64_t q = threadIdx.x; q < npx; q += kT) atomicAdd(&h[p[q]], 1u);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint64_t cum = 0;
-    int T = 0;
-    for (int v = 255; v >= 0; --v) {
-      if (cum + h[v] >= (uint64_t)K) { T = v; break; }
-      cum += h[v];
+  uint32_t* hw = h[wid];
+  if (VEC) {
+    const int64_t U = npx / 16, u0 = U * part / kFullParts, u1 = U * (part + 1) / kFullParts;
+    for (int64_t u = u0 + threadIdx.x; u < u1; u += kT) {
+      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(p) + u);
+      const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 16; ++q) atomicAdd(&hw[(ws[q >> 2] >> (8 * (q & 3))) & 0xFFu], 1u);
     }
-    T_s = (uint32_t)T;
-    sel[f].T = (uint32_t)T;
-    sel[f].above = (uint32_t)cum;
-    sel[f].mode = kSelFast;
+  } else {
+    const int64_t q0 = npx * part / kFullParts, q1 = npx * (part + 1) / kFullParts;
+    for (int64_t q = q0 + threadIdx.x; q < q1; q += kT) atomicAdd(&hw[p[q]], 1u);
   }
   __syncthreads();
-  const uint32_t T = T_s;
-  // per-row counts, warp per row, into row_info[.].x/.y, then prefixes
+  for (int b = threadIdx.x; b < 256; b += kT) {
+    uint32_t c = 0;
+    for (int w = 0; w < kWarps; ++w) c += h[w][b];
+    if (c) atomicAdd(hist256 + (int64_t)f * 256 + b, c);
+  }
+  (void)lane;
+}
+
+// F2: threshold from the full histogram.
+__global__ void __launch_bounds__(32)
+k_full_threshold(int64_t K, FrameSel* __restrict__ sel, const uint32_t* __restrict__ hist256) {
+  const int f = blockIdx.x;
+  if (threadIdx.x != 0 || sel[f].mode != kSelFull) return;
+  uint64_t cum = 0;
+  int T = 0;
+  for (int v = 255; v >= 0; --v) {
+    const uint32_t c = hist256[(int64_t)f * 256 + v];
+    if (cum + c >= (uint64_t)K) {
+      T = v;
+      break;
+    }
+    cum += c;
+  }
+  sel[f].T = (uint32_t)T;
+  sel[f].above = (uint32_t)cum;
+}
+
+// F3: per-row (above, tie) counts, warp per row, rows spread over kFullParts CTAs.
+__global__ void __launch_bounds__(kT)
+k_full_rows(const uint8_t* __restrict__ dark, int64_t dark_fs, int H, int W, const FrameSel* __restrict__ sel,
+            uint32_t* __restrict__ row_info) {
+  const int f = blockIdx.y, part = blockIdx.x;
+  if (sel[f].mode != kSelFull) return;
+  const uint32_t T = sel[f].T;
+  const uint8_t* p = dark + f * dark_fs;
   uint4* info = reinterpret_cast<uint4*>(row_info + (int64_t)f * H * 4);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int y = wid; y < H; y += kWarps) {
+  for (int y = part * kWarps + wid; y < H; y += kWarps * kFullParts) {
     uint32_t na = 0, nt = 0;
     for (int x = lane; x < W; x += 32) {
       const uint32_t b = p[(int64_t)y * W + x];
@@ -223,12 +261,21 @@ k_threshold_full(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx,
     }
     if (lane == 0) info[y] = make_uint4(na, nt, 0u, 0u);
   }
-  __syncthreads();
+}
+
+// F4: exclusive prefixes of the per-row counts; the frame joins the fast path.
+__global__ void __launch_bounds__(kT)
+k_full_scan(int H, FrameSel* __restrict__ sel, uint32_t* __restrict__ row_info) {
+  const int f = blockIdx.x;
+  if (sel[f].mode != kSelFull) return;
+  uint4* info = reinterpret_cast<uint4*>(row_info + (int64_t)f * H * 4);
   scan_rows(H, row_info + (int64_t)f * H * 4, [&](int y, uint32_t& a, uint32_t& t) {
     const uint4 v = info[y];
     a = v.x;
     t = v.y;
   });
+  __syncthreads();
+  if (threadIdx.x == 0) sel[f].mode = kSelFast;
 }
 
 // ---------------------------------------------------------------------------
@@ -282,34 +329,44 @@ __device__ void compact_row(const uint8_t* __restrict__ row, int W, uint32_t bas
   }
 }
 
+// The gather of chunk c+1 (warps 1..7) overlaps the sequential sums of chunk c
+// (lanes 0..2 of warp 0), so large K is bound by the three dependent fp64 chains.
 __device__ void airlight_sum(const uint8_t* __restrict__ frame, const uint32_t* __restrict__ idx, int64_t K,
                              bool all, double alpha, double* __restrict__ A) {
   constexpr int kChunk = 2048;
   __shared__ double tab[256];
-  __shared__ uint32_t buf[kChunk];
+  __shared__ uint32_t buf[2][kChunk];
   for (int v = threadIdx.x; v < 256; v += kT) tab[v] = __ddiv_rn((double)v, 255.0);
-  double acc = 0.0;
-  const int sh = 8 * (threadIdx.x < 3 ? threadIdx.x : 0);
-  for (int64_t base = 0; base < K; base += kChunk) {
+  auto gather = [&](int64_t base, uint32_t* dst, int t0, int stride) {
     const int cnt = (int)min((int64_t)kChunk, K - base);
-    __syncthreads();
-    for (int e = threadIdx.x; e < cnt; e += kT) {
+    for (int e = t0; e < cnt; e += stride) {
       const int64_t px = all ? base + e : (int64_t)__ldcg(idx + base + e);
       const uint8_t* q = frame + 3 * px;
-      buf[e] = (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16);
+      dst[e] = (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16);
     }
-    __syncthreads();
-    if (threadIdx.x < 3) {  // lanes 0..2 of warp 0: one sequential chain per channel
+  };
+  gather(0, buf[0], threadIdx.x, kT);
+  __syncthreads();
+  double acc = 0.0;
+  const int sh = 8 * (threadIdx.x < 3 ? threadIdx.x : 0);
+  int cur = 0;
+  for (int64_t base = 0; base < K; base += kChunk, cur ^= 1) {
+    const int cnt = (int)min((int64_t)kChunk, K - base);
+    if (threadIdx.x >= 32) {
+      if (base + kChunk < K) gather(base + kChunk, buf[cur ^ 1], threadIdx.x - 32, kT - 32);
+    } else if (threadIdx.x < 3) {  // lanes 0..2 of warp 0: one sequential chain per channel
+      const uint32_t* b = buf[cur];
       int e = 0;
       for (; e + 8 <= cnt; e += 8) {
         double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = tab[(buf[e + u] >> sh) & 0xFFu];
+        for (int u = 0; u < 8; ++u) v[u] = tab[(b[e + u] >> sh) & 0xFFu];
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
       }
-      for (; e < cnt; ++e) acc = __dadd_rn(acc, tab[(buf[e] >> sh) & 0xFFu]);
+      for (; e < cnt; ++e) acc = __dadd_rn(acc, tab[(b[e] >> sh) & 0xFFu]);
     }
+    __syncthreads();
   }
   if (threadIdx.x < 3) {
     const double mean = __ddiv_rn(acc, (double)K);
@@ -373,14 +430,16 @@ cudaError_t select_u8(const uint8_t* dark, int64_t dark_fs, const uint8_t* in, i
                                            ws.frame_hist);
   }
   k_threshold<<<n, kT, 0, st>>>(npx, K, H, ws.frame_max, ws.row_hist, ws.frame_hist, ws.sel, ws.row_info);
-  const dim3 cgrid(kCompactParts, n);
-  if (vec) {
-    k_threshold_full<true><<<n, kT, 0, st>>>(dark, dark_fs, npx, K, H, W, ws.sel, ws.row_info);
+  const dim3 cgrid(kCompactParts, n), fgrid(kFullParts, n);
+  if (vec) k_full_hist<true><<<fgrid, kT, 0, st>>>(dark, dark_fs, npx, ws.sel, ws.hist256);
+  else k_full_hist<false><<<fgrid, kT, 0, st>>>(dark, dark_fs, npx, ws.sel, ws.hist256);
+  k_full_threshold<<<n, 32, 0, st>>>(K, ws.sel, ws.hist256);
+  k_full_rows<<<fgrid, kT, 0, st>>>(dark, dark_fs, H, W, ws.sel, ws.row_info);
+  k_full_scan<<<n, kT, 0, st>>>(H, ws.sel, ws.row_info);
+  if (vec)
     k_compact<true><<<cgrid, kT, 0, st>>>(dark, dark_fs, npx, K, H, W, ws.sel, ws.row_info, ws.sel_idx);
-  } else {
-    k_threshold_full<false><<<n, kT, 0, st>>>(dark, dark_fs, npx, K, H, W, ws.sel, ws.row_info);
+  else
     k_compact<false><<<cgrid, kT, 0, st>>>(dark, dark_fs, npx, K, H, W, ws.sel, ws.row_info, ws.sel_idx);
-  }
   k_airlight<<<n, kT, 0, st>>>(in, in_fs, K, alpha, ws.sel, ws.sel_idx, airlight);
   return cudaGetLastError();
 }
