@@ -16,7 +16,8 @@ constexpr int kTri = 256 * 257 / 2;  // 32896
 // Per-frame recovery table (K5 writes it, K6 stages it in shared memory): three
 // triangular planes, entry (i, m <= i) of channel c at c*kTri + i*(i+1)/2 + m.
 // (A 260-byte-pitch square layout has ~12% fewer bank conflicts but needs 196 KB,
-// i.e. one CTA per SM, and measured slower than two 99 KB CTAs per SM.)
+// i.e. one CTA per SM: with or without the diagonal split of K6 it measured slower,
+// since pitch-260 rows put neighbouring (i, m) entries into neighbouring banks.)
 constexpr int kLutFrame = 3 * kTri;  // 98688 bytes, 16-byte multiple
 
 // Width of the max-relative window histogram used by the fast select path.
