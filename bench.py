@@ -363,9 +363,9 @@ def main():
                 "traffic": None if t_px is None else int(t_px * n * npx), "peak_kind": peak_kind,
                 "alg_bytes_per_launch": rec_bytes, "launch_ms": round(stage_ms[3], 4),
                 "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read+write per px)"}
-        # K1, K2 level hist, K3 threshold, 4 fallback kernels (exit at once on the fast
+        # K1, K2 level hist, K3 threshold, 2 fallback kernels (exit at once on the fast
         # path), K3c compact, K4 airlight, K5 LUT (balance: g table, sums, LUT), K6
-        launches = 11 + (2 if params.balance_enabled() else 0)
+        launches = 9 + (2 if params.balance_enabled() else 0)
     elif native:
         gb = GUIDED_BYTES[params.balance_enabled()] * n * npx
         g_gbs = gb / (stage_ms[2] / 1000.0) / 1e9
@@ -373,8 +373,8 @@ def main():
                 "achieved": round(g_gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(g_gbs / peak, 4),
                 "traffic": None, "peak_kind": peak_kind, "alg_bytes_per_launch": gb,
                 "launch_ms": round(stage_ms[2], 4)}
-        # K1 + the 8 select kernels + pass1 + pass2 (+ thresholds + apply) per <=4 GB chunk of frames
-        launches = 9 + (4 if params.balance_enabled() else 2) * math.ceil(n / _guided_chunk(n, H, W, params))
+        # K1 + the 6 select kernels + pass1 + pass2 (+ thresholds + apply) per <=4 GB chunk of frames
+        launches = 7 + (4 if params.balance_enabled() else 2) * math.ceil(n / _guided_chunk(n, H, W, params))
     else:
         roof = {"bound": "hbm", "kernel": "float64 image-mode pipeline (whole step)", "achieved": round(pipe_gbs, 1),
                 "peak": peak, "unit": "GB/s", "frac": round(pipe_gbs / peak, 4), "traffic": None,

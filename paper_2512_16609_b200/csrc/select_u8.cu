@@ -18,8 +18,9 @@
 // K3 (k_threshold): CTA per frame: T = K-th largest level, per-row (above,
 //   tie) counts and their exclusive prefixes over rows (linear index order).
 //   Frames whose top K spans more than 16 levels are redone by K3b
-//   (k_full_hist/_threshold/_rows/_scan: a full 256-level histogram and per-row
-//   counts spread over many CTAs per frame; frames on the fast path exit at once).
+//   (k_full_hist / k_full_rows: a full 256-level histogram and per-row counts
+//   spread over many CTAs per frame, the last CTA of each finishing the frame's
+//   step; frames on the fast path exit at once).
 // K4 (k_compact_sum): CTA per frame: warps compact the few rows that hold
 //   selected pixels (ballot-free: per-lane counts + warp scan, index order),
 //   then the gather and the three sequential fp64 channel sums.
@@ -184,15 +185,17 @@ k_threshold(int64_t npx, int64_t K, int H, const uint32_t* __restrict__ frame_ma
 // spread over kFullParts CTAs per frame (frames on the fast path exit at once).
 constexpr int kFullParts = 32;
 
-// F1: 256-level histogram of the frame's dark bytes (warp-private shared copies).
+// F1: 256-level histogram of the frame's dark bytes (warp-private shared copies);
+// the frame's last CTA to finish (ticket) derives T and the count above it.
 template <bool VEC>
 __global__ void __launch_bounds__(kT)
-k_full_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, const FrameSel* __restrict__ sel,
+k_full_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_t K, FrameSel* __restrict__ sel,
             uint32_t* __restrict__ hist256) {
   const int f = blockIdx.y, part = blockIdx.x;
   if (sel[f].mode != kSelFull) return;
   __shared__ uint32_t h[kWarps][256];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ bool last;
+  const int wid = threadIdx.x >> 5;
   for (int k = threadIdx.x; k < kWarps * 256; k += kT) (&h[0][0])[k] = 0;
   __syncthreads();
   const uint8_t* p = dark + f * dark_fs;
@@ -210,23 +213,22 @@ k_full_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, cons
     for (int64_t q = q0 + threadIdx.x; q < q1; q += kT) atomicAdd(&hw[p[q]], 1u);
   }
   __syncthreads();
+  uint32_t* fh = hist256 + (int64_t)f * 256;
   for (int b = threadIdx.x; b < 256; b += kT) {
     uint32_t c = 0;
     for (int w = 0; w < kWarps; ++w) c += h[w][b];
-    if (c) atomicAdd(hist256 + (int64_t)f * 256 + b, c);
+    if (c) atomicAdd(fh + b, c);
   }
-  (void)lane;
-}
-
-// F2: threshold from the full histogram.
-__global__ void __launch_bounds__(32)
-k_full_threshold(int64_t K, FrameSel* __restrict__ sel, const uint32_t* __restrict__ hist256) {
-  const int f = blockIdx.x;
-  if (threadIdx.x != 0 || sel[f].mode != kSelFull) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&sel[f].ticket, 1u) == kFullParts - 1;
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
   uint64_t cum = 0;
   int T = 0;
   for (int v = 255; v >= 0; --v) {
-    const uint32_t c = hist256[(int64_t)f * 256 + v];
+    const uint32_t c = __ldcg(fh + v);
     if (cum + c >= (uint64_t)K) {
       T = v;
       break;
@@ -237,13 +239,15 @@ k_full_threshold(int64_t K, FrameSel* __restrict__ sel, const uint32_t* __restri
   sel[f].above = (uint32_t)cum;
 }
 
-// F3: per-row (above, tie) counts, warp per row, rows spread over kFullParts CTAs.
+// F2: per-row (above, tie) counts, warp per row, rows spread over kFullParts CTAs; the
+// frame's last CTA writes the exclusive prefixes and moves the frame to the fast path.
 __global__ void __launch_bounds__(kT)
-k_full_rows(const uint8_t* __restrict__ dark, int64_t dark_fs, int H, int W, const FrameSel* __restrict__ sel,
+k_full_rows(const uint8_t* __restrict__ dark, int64_t dark_fs, int H, int W, FrameSel* __restrict__ sel,
             uint32_t* __restrict__ row_info) {
   const int f = blockIdx.y, part = blockIdx.x;
   if (sel[f].mode != kSelFull) return;
-  const uint32_t T = sel[f].T;
+  __shared__ bool last;
+  const uint32_t T = __ldcg(&sel[f].T);
   const uint8_t* p = dark + f * dark_fs;
   uint4* info = reinterpret_cast<uint4*>(row_info + (int64_t)f * H * 4);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -261,16 +265,14 @@ k_full_rows(const uint8_t* __restrict__ dark, int64_t dark_fs, int H, int W, con
     }
     if (lane == 0) info[y] = make_uint4(na, nt, 0u, 0u);
   }
-}
-
-// F4: exclusive prefixes of the per-row counts; the frame joins the fast path.
-__global__ void __launch_bounds__(kT)
-k_full_scan(int H, FrameSel* __restrict__ sel, uint32_t* __restrict__ row_info) {
-  const int f = blockIdx.x;
-  if (sel[f].mode != kSelFull) return;
-  uint4* info = reinterpret_cast<uint4*>(row_info + (int64_t)f * H * 4);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&sel[f].ticket2, 1u) == kFullParts - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
   scan_rows(H, row_info + (int64_t)f * H * 4, [&](int y, uint32_t& a, uint32_t& t) {
-    const uint4 v = info[y];
+    const uint4 v = __ldcg(info + y);
     a = v.x;
     t = v.y;
   });
@@ -431,11 +433,9 @@ cudaError_t select_u8(const uint8_t* dark, int64_t dark_fs, const uint8_t* in, i
   }
   k_threshold<<<n, kT, 0, st>>>(npx, K, H, ws.frame_max, ws.row_hist, ws.frame_hist, ws.sel, ws.row_info);
   const dim3 cgrid(kCompactParts, n), fgrid(kFullParts, n);
-  if (vec) k_full_hist<true><<<fgrid, kT, 0, st>>>(dark, dark_fs, npx, ws.sel, ws.hist256);
-  else k_full_hist<false><<<fgrid, kT, 0, st>>>(dark, dark_fs, npx, ws.sel, ws.hist256);
-  k_full_threshold<<<n, 32, 0, st>>>(K, ws.sel, ws.hist256);
+  if (vec) k_full_hist<true><<<fgrid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.sel, ws.hist256);
+  else k_full_hist<false><<<fgrid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.sel, ws.hist256);
   k_full_rows<<<fgrid, kT, 0, st>>>(dark, dark_fs, H, W, ws.sel, ws.row_info);
-  k_full_scan<<<n, kT, 0, st>>>(H, ws.sel, ws.row_info);
   if (vec)
     k_compact<true><<<cgrid, kT, 0, st>>>(dark, dark_fs, npx, K, H, W, ws.sel, ws.row_info, ws.sel_idx);
   else
