@@ -51,7 +51,7 @@ int64_t align_up(int64_t v, int64_t a = kAlign) { return (v + a - 1) / a * a; }
 
 struct Layout {
   // [0, zero_end) is cleared at the start of every call
-  int64_t frame_max, sel, blk_max, row_hist, frame_hist, hist256, zero_end;
+  int64_t frame_max, sel, unit_max, row_hist, frame_hist, hist256, full_list, zero_end;
   int64_t row_info, sel_idx, lut, bal, dark, tmap, total;
   int64_t dark_fs;
 };
@@ -66,13 +66,14 @@ Layout make_layout(int n, int H, int W, const dhz_params* p) {
     o = align_up(o + bytes);
     return at;
   };
-  const int64_t nb = (H + dhz::kBandH - 1) / dhz::kBandH, ntx = (W + dhz::kBandW - 1) / dhz::kBandW;
+  const int64_t nb = (H + dhz::kBandH - 1) / dhz::kBandH, nu = (W + dhz::kUnitW - 1) / dhz::kUnitW;
   L.frame_max = take(4LL * n);
   L.sel = take((int64_t)sizeof(dhz::FrameSel) * n);
-  L.blk_max = take(4LL * n * nb * ntx);
+  L.unit_max = take(4LL * n * nb * nu);
   L.row_hist = take(4LL * dhz::kWin * n * H);
   L.frame_hist = take(4LL * dhz::kWin * n);
   L.hist256 = take(4LL * 256 * n);
+  L.full_list = take(4LL * (n + 1));
   L.zero_end = o;
   L.row_info = take(16LL * n * H);
   L.sel_idx = take(4LL * n * std::max<int64_t>(1, p->top_k));
@@ -167,18 +168,19 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const d
 
   uint8_t* dark = base + L.dark;
   uint32_t* fmax = reinterpret_cast<uint32_t*>(base + L.frame_max);
-  uint32_t* bmax = reinterpret_cast<uint32_t*>(base + L.blk_max);
-  e = dhz::dark_u8(in, in_fs, n, H, W, p->patch_radius, dark, L.dark_fs, fmax, bmax, st);
+  uint32_t* umax = reinterpret_cast<uint32_t*>(base + L.unit_max);
+  e = dhz::dark_u8(in, in_fs, n, H, W, p->patch_radius, dark, L.dark_fs, fmax, umax, st);
   if (e != cudaSuccess) return cuda_fail(e, "dark_u8");
   mark(1);
 
   dhz::SelectWs sw{};
   sw.sel = reinterpret_cast<dhz::FrameSel*>(base + L.sel);
   sw.frame_max = fmax;
-  sw.blk_max = bmax;
+  sw.unit_max = umax;
   sw.row_hist = reinterpret_cast<uint32_t*>(base + L.row_hist);
   sw.frame_hist = reinterpret_cast<uint32_t*>(base + L.frame_hist);
   sw.hist256 = reinterpret_cast<uint32_t*>(base + L.hist256);
+  sw.full_list = reinterpret_cast<uint32_t*>(base + L.full_list);
   sw.row_info = reinterpret_cast<uint32_t*>(base + L.row_info);
   sw.sel_idx = reinterpret_cast<uint32_t*>(base + L.sel_idx);
   sw.H = H;

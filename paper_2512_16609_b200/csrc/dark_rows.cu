@@ -14,8 +14,9 @@
 //    supply halo, so a warp yields 480 pixels; the row goes to shared memory.
 //  pass 2 (thread per 4 columns x 16 rows): vertical window min of the
 //    shared rows in registers and a coalesced 4-byte store per row, plus the
-//    max over each 16-row x 480-column block (blk_max[], frame_max[]) that lets the top-K
-//    select skip bands that cannot hold selected pixels.
+//    max over each 16-row x 32-column unit (unit_max[], from per-item maxima)
+//    and per frame (frame_max[]) that let the top-K select skip units that cannot
+//    hold selected pixels.
 #include "dhz_common.cuh"
 #include "dhz_internal.h"
 
@@ -25,7 +26,7 @@ namespace {
 
 constexpr int kTW = kBandW;  // output columns per tile (30 lanes x 16 px)
 constexpr int kBH = 64;    // output rows per tile
-constexpr int kRun = kBandH;  // rows per pass-2 item (== block height of blk_max)
+constexpr int kRun = kBandH;  // rows per pass-2 item (== unit height of unit_max)
 constexpr int kThreads = 256;
 #ifndef DHZ_K1_MINB
 #define DHZ_K1_MINB 4  // resident CTAs per SM the register budget is sized for
@@ -85,16 +86,14 @@ __device__ __forceinline__ uint32_t vert_final(const uint32_t (&v)[N], int j) {
 template <int R>
 __global__ void __launch_bounds__(kThreads, R <= 8 ? DHZ_K1_MINB : 1)
 k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t* __restrict__ dark,
-            int64_t dark_fs, uint32_t* __restrict__ frame_max, uint32_t* __restrict__ blk_max) {
+            int64_t dark_fs, uint32_t* __restrict__ frame_max, uint32_t* __restrict__ unit_max) {
   using G = RowGeo<R>;
   constexpr int L = G::L, P = G::P, HPR = G::HPR, NP = G::NP;
   extern __shared__ __align__(16) uint8_t hrow[];  // [ROWS][kTW] horizontal minima
-  __shared__ uint32_t run_max[kBH / kRun];
   const int f = blockIdx.z;
   const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kBH;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint8_t* frame = in + (int64_t)f * in_fs;
-  if (threadIdx.x < kBH / kRun) run_max[threadIdx.x] = 0;
 
   // ---------------- pass 1: channel min + horizontal min, warp per row ----------------
   const int x = x0 - 16 + 16 * lane;  // first pixel of this lane
@@ -169,8 +168,10 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
   constexpr int NG = kTW / 4;                 // 120 column groups
   // the warp shuffles below need whole warps in every iteration of the item loop
   static_assert((NG * (kBH / kRun)) % 32 == 0, "pass-2 items must fill whole warps");
+  static_assert(NG % 8 == 0 && kTW % kUnitW == 0 && kRun == kBandH, "unit maxima: 8 groups of 4 columns");
+  static_assert(((kTW / kUnitW) * (kBH / kRun) + 31) / 32 * 32 <= kThreads, "one thread per unit");
   constexpr int N = kRun + 2 * R;
-  uint32_t tmax = 0;
+  __shared__ __align__(16) uint32_t item_max[NG * (kBH / kRun)];
   for (int it = threadIdx.x; it < NG * (kBH / kRun); it += kThreads) {
     const int run = it / NG, g = it - run * NG;
     const int j0 = run * kRun;
@@ -206,38 +207,39 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
         }
       }
     }
-    mx = max(mx & 0xFFFFu, mx >> 16);
-#pragma unroll
-    for (int sh = 16; sh > 0; sh >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, sh));
-    // a warp's 32 consecutive items may straddle two runs: fold the warp max into both
-    const int run_first = __shfl_sync(0xffffffffu, run, 0);
-    if (lane == 0) atomicMax(&run_max[run_first], mx);
-    if (lane == 31 && run != run_first) atomicMax(&run_max[run], mx);
-    tmax = max(tmax, mx);
+    item_max[it] = max(mx & 0xFFFFu, mx >> 16);
   }
   __syncthreads();
-  if (threadIdx.x < kBH / kRun) {  // max per (16-row band, 480-col tile), owned by this CTA
-    const int band = (y0 / kRun) + threadIdx.x;
-    if (y0 + threadIdx.x * kRun < H)
-      blk_max[((int64_t)f * ((H + kBandH - 1) / kBandH) + band) * ((W + kBandW - 1) / kBandW) + blockIdx.x] =
-          run_max[threadIdx.x];
-  }
-  if (threadIdx.x == 0) {
-    uint32_t m = 0;
-    for (int i = 0; i < kBH / kRun; ++i) m = max(m, run_max[i]);
-    atomicMax(frame_max + f, m);
+  // unit maxima (8 column groups of 4 = 32 columns) and the frame maximum
+  constexpr int NU = kTW / kUnitW;  // 15 units per tile row
+  constexpr int NUT = NU * (kBH / kRun);
+  if (threadIdx.x < (NUT + 31) / 32 * 32) {  // whole warps: the shuffles below need them
+    uint32_t um = 0;
+    if (threadIdx.x < NUT) {
+      const int run = threadIdx.x / NU, u = threadIdx.x - run * NU;
+      const uint4 a = *reinterpret_cast<const uint4*>(&item_max[run * NG + 8 * u]);
+      const uint4 b = *reinterpret_cast<const uint4*>(&item_max[run * NG + 8 * u + 4]);
+      um = max(max(max(a.x, a.y), max(a.z, a.w)), max(max(b.x, b.y), max(b.z, b.w)));
+      const int xu = x0 + kUnitW * u, yr = y0 + run * kRun;
+      if (xu < W && yr < H)
+        unit_max[((int64_t)f * ((H + kBandH - 1) / kBandH) + yr / kBandH) * ((W + kUnitW - 1) / kUnitW) +
+                 xu / kUnitW] = um;
+    }
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) um = max(um, __shfl_xor_sync(0xffffffffu, um, sh));
+    if (lane == 0 && um) atomicMax(frame_max + f, um);
   }
 }
 
 template <int R>
 cudaError_t launch(const uint8_t* in, int64_t in_fs, int n, int H, int W, uint8_t* dark, int64_t dark_fs,
-                   uint32_t* frame_max, uint32_t* blk_max, cudaStream_t st) {
+                   uint32_t* frame_max, uint32_t* unit_max, cudaStream_t st) {
   using G = RowGeo<R>;
   auto kern = k_dark_rows<R>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
   if (e != cudaSuccess) return e;
   dim3 grid((W + kTW - 1) / kTW, (H + kBH - 1) / kBH, n);
-  kern<<<grid, kThreads, G::SMEM, st>>>(in, in_fs, H, W, dark, dark_fs, frame_max, blk_max);
+  kern<<<grid, kThreads, G::SMEM, st>>>(in, in_fs, H, W, dark, dark_fs, frame_max, unit_max);
   return cudaGetLastError();
 }
 
@@ -249,11 +251,11 @@ bool dark_rows_supported(int r, int W, int64_t in_fs, int64_t dark_fs, const voi
 }
 
 cudaError_t dark_rows(const uint8_t* in, int64_t in_fs, int n, int H, int W, int r, uint8_t* dark,
-                      int64_t dark_fs, uint32_t* frame_max, uint32_t* blk_max, cudaStream_t st) {
+                      int64_t dark_fs, uint32_t* frame_max, uint32_t* unit_max, cudaStream_t st) {
   switch (r) {
 #define DHZ_R(k) \
   case k:        \
-    return launch<k>(in, in_fs, n, H, W, dark, dark_fs, frame_max, blk_max, st);
+    return launch<k>(in, in_fs, n, H, W, dark, dark_fs, frame_max, unit_max, st);
     DHZ_R(1) DHZ_R(2) DHZ_R(3) DHZ_R(4) DHZ_R(5) DHZ_R(6) DHZ_R(7) DHZ_R(8)
     DHZ_R(9) DHZ_R(10) DHZ_R(11) DHZ_R(12) DHZ_R(13) DHZ_R(14) DHZ_R(15) DHZ_R(16)
 #undef DHZ_R

@@ -173,7 +173,7 @@ template <bool VEC, int R>
 __global__ void __launch_bounds__(kThreads)
 k_dark_u8(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r,
           uint8_t* __restrict__ dark, int64_t dark_fs, uint32_t* __restrict__ frame_max,
-          uint32_t* __restrict__ row_max) {
+          uint32_t* __restrict__ unit_max) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int f = blockIdx.z;
   const int x0 = blockIdx.x * kSW;
@@ -242,8 +242,8 @@ k_dark_u8(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r,
     {
       const uint32_t cm = max(max(tmax & 0xFFu, (tmax >> 8) & 0xFFu), max((tmax >> 16) & 0xFFu, tmax >> 24));
       if (x < W)
-        atomicMax(row_max + ((int64_t)f * ((H + kBandH - 1) / kBandH) + y / kBandH) * ((W + kBandW - 1) / kBandW) +
-                      x / kBandW,
+        atomicMax(unit_max + ((int64_t)f * ((H + kBandH - 1) / kBandH) + y / kBandH) * ((W + kUnitW - 1) / kUnitW) +
+                      x / kUnitW,
                   cm);
       tmax = vmax4(tmax, tmax_before);
     }
@@ -264,7 +264,7 @@ k_dark_u8(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r,
 
 template <bool VEC, int R>
 cudaError_t launch_dark(const uint8_t* in, int64_t in_fs, int n, int H, int W, int r, uint8_t* dark,
-                        int64_t dark_fs, uint32_t* frame_max, uint32_t* row_max, cudaStream_t st) {
+                        int64_t dark_fs, uint32_t* frame_max, uint32_t* unit_max, cudaStream_t st) {
   const int rr = R > 0 ? R : r;
   const int HP = halo_px(rr);
   const int LW = kSW + 2 * HP;
@@ -273,7 +273,7 @@ cudaError_t launch_dark(const uint8_t* in, int64_t in_fs, int n, int H, int W, i
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((W + kSW - 1) / kSW, (H + kBH - 1) / kBH, n);
-  kern<<<grid, kThreads, smem, st>>>(in, in_fs, H, W, r, dark, dark_fs, frame_max, row_max);
+  kern<<<grid, kThreads, smem, st>>>(in, in_fs, H, W, r, dark, dark_fs, frame_max, unit_max);
   return cudaGetLastError();
 }
 
@@ -286,14 +286,14 @@ size_t dark_u8_max_smem(int r) {
 }
 
 cudaError_t dark_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, int r, uint8_t* dark,
-                    int64_t dark_fs, uint32_t* frame_max, uint32_t* row_max, cudaStream_t st) {
+                    int64_t dark_fs, uint32_t* frame_max, uint32_t* unit_max, cudaStream_t st) {
   if (dark_rows_supported(r, W, in_fs, dark_fs, in, dark))
-    return dark_rows(in, in_fs, n, H, W, r, dark, dark_fs, frame_max, row_max, st);
+    return dark_rows(in, in_fs, n, H, W, r, dark, dark_fs, frame_max, unit_max, st);
   const bool vec = (W % 16 == 0) && (in_fs % 16 == 0) && (dark_fs % 16 == 0) &&
                    ((uintptr_t)in % 16 == 0) && ((uintptr_t)dark % 16 == 0);
-  if (vec) return launch_dark<true, 0>(in, in_fs, n, H, W, r, dark, dark_fs, frame_max, row_max, st);
-  if (r == 7) return launch_dark<false, 7>(in, in_fs, n, H, W, r, dark, dark_fs, frame_max, row_max, st);
-  return launch_dark<false, 0>(in, in_fs, n, H, W, r, dark, dark_fs, frame_max, row_max, st);
+  if (vec) return launch_dark<true, 0>(in, in_fs, n, H, W, r, dark, dark_fs, frame_max, unit_max, st);
+  if (r == 7) return launch_dark<false, 7>(in, in_fs, n, H, W, r, dark, dark_fs, frame_max, unit_max, st);
+  return launch_dark<false, 0>(in, in_fs, n, H, W, r, dark, dark_fs, frame_max, unit_max, st);
 }
 
 }  // namespace dhz

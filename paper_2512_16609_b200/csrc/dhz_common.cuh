@@ -23,8 +23,10 @@ constexpr int kLutFrame = 3 * kTri;  // 98688 bytes, 16-byte multiple
 // Width of the max-relative window histogram used by the fast select path.
 constexpr int kWin = 16;
 
-// Dark-map blocks whose maxima K1 records for the select pass (16 rows x 480 columns).
+// K1 records the maximum of every 16-row x 32-column unit of the dark map; the
+// select pass reads only the units that can hold top-K pixels.  (480: K1's tile width.)
 constexpr int kBandH = 16;
+constexpr int kUnitW = 32;
 constexpr int kBandW = 480;
 
 __device__ __forceinline__ uint32_t vmin4(uint32_t a, uint32_t b) { return __vminu4(a, b); }

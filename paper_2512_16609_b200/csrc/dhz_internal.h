@@ -26,21 +26,22 @@ enum : uint32_t { kSelFast = 0, kSelFull = 1, kSelAll = 2 };
 // K1: dark map (u8) + per-frame max.  dark_fs/in_fs are byte strides between frames.
 cudaError_t dark_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, int r, uint8_t* dark,
                     int64_t dark_fs, uint32_t* frame_max /* [n], zeroed by the caller */,
-                    uint32_t* blk_max /* [n][ceil(H/16)][ceil(W/480)], zeroed by the caller */,
+                    uint32_t* unit_max /* [n][ceil(H/16)][ceil(W/32)], zeroed by the caller */,
                     cudaStream_t st);
 bool dark_rows_supported(int r, int W, int64_t in_fs, int64_t dark_fs, const void* in, const void* dark);
 cudaError_t dark_rows(const uint8_t* in, int64_t in_fs, int n, int H, int W, int r, uint8_t* dark,
-                      int64_t dark_fs, uint32_t* frame_max, uint32_t* blk_max, cudaStream_t st);
+                      int64_t dark_fs, uint32_t* frame_max, uint32_t* unit_max, cudaStream_t st);
 size_t dark_u8_max_smem(int r);
 
 // K2/K3: ordered top-K select on the u8 dark map and the sequential fp64 airlight sum.
 struct SelectWs {
   FrameSel* sel;         // [n]
   uint32_t* frame_max;   // [n]  (K1 output)
-  uint32_t* blk_max;     // [n][ceil(H/16)][ceil(W/480)] max dark value per block (K1 output)
+  uint32_t* unit_max;    // [n][ceil(H/16)][ceil(W/32)] max dark value per unit (K1 output)
   uint32_t* row_hist;    // [n][H][16] pixels per row at level max-j, zeroed by the caller
   uint32_t* frame_hist;  // [n][16], zeroed by the caller
   uint32_t* hist256;     // [n][256] full level histogram (fallback frames only), zeroed by the caller
+  uint32_t* full_list;   // [n + 1]: count, then the frames on the fallback path; zeroed by the caller
   uint32_t* row_info;    // [n][H][4] = above, ties, above_prefix, tie_prefix
   uint32_t* sel_idx;     // [n][K] selected flat indices in summation order
   int H, W;

@@ -11,9 +11,9 @@
 // chain exactly, so A is bit-identical to the reference.  When K == n the
 // reference takes arange(n) (:75-76).
 //
-// K2 (k_level_hist): warp per 16-row x 480-column dark block.  Blocks whose
-//   maximum (recorded by K1) is below max-15 are skipped without reading; the
-//   others count the pixels of each level in [max-15, max] per row (rare
+// K2 (k_level_hist): K1 recorded the maximum of every 16-row x 32-column unit;
+//   units below max-15 are skipped without reading (one gather tests 32 units),
+//   the others count the pixels of each level in [max-15, max] per row (rare
 //   shared atomics), folded into a per-row / per-frame level histogram.
 // K3 (k_threshold): CTA per frame: T = K-th largest level, per-row (above,
 //   tie) counts and their exclusive prefixes over rows (linear index order).
@@ -21,9 +21,9 @@
 //   (k_full_hist / k_full_rows: a full 256-level histogram and per-row counts
 //   spread over many CTAs per frame, the last CTA of each finishing the frame's
 //   step; frames on the fast path exit at once).
-// K4 (k_compact_sum): CTA per frame: warps compact the few rows that hold
-//   selected pixels (ballot-free: per-lane counts + warp scan, index order),
-//   then the gather and the three sequential fp64 channel sums.
+// K4 (k_compact, k_airlight): warps compact the rows that hold selected pixels,
+//   reading only the row's units whose maximum reaches T (ballot + popc, index
+//   order); then a CTA per frame gathers and runs the three sequential fp64 sums.
 #include "dhz_common.cuh"
 #include "dhz_internal.h"
 
@@ -34,81 +34,98 @@ namespace {
 constexpr int kT = 256;
 constexpr int kWarps = kT / 32;
 
-__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, int lane, uint32_t* total) {
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  *total = __shfl_sync(0xffffffffu, x, 31);
-  return x - v;
-}
-
 // ---------------------------------------------------------------------------
 // K2: per-row level histogram of the levels [M-15, M]
 // ---------------------------------------------------------------------------
+// One 16 x 32 unit: count its pixels in [L, M] per (row, level) on the warp's shared
+// counters, then fold them into the per-row and per-frame histograms (and re-zero).
 template <bool VEC>
-__global__ void __launch_bounds__(kT)
-k_level_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int n, int H, int W,
-             const uint32_t* __restrict__ frame_max, const uint32_t* __restrict__ blk_max,
-             uint32_t* __restrict__ row_hist /* [n][H][16] */, uint32_t* __restrict__ frame_hist /* [n][16] */) {
-  __shared__ uint32_t cnt[kWarps][kBandH][kWin];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nb = (H + kBandH - 1) / kBandH, ntx = (W + kBandW - 1) / kBandW;
-  const int64_t items = (int64_t)n * nb * ntx;
-  uint32_t* c = &cnt[wid][0][0];
-  for (int64_t it = (int64_t)blockIdx.x * kWarps + wid; it < items; it += (int64_t)gridDim.x * kWarps) {
-    const int f = (int)(it / ((int64_t)nb * ntx));
-    const int rem = (int)(it - (int64_t)f * nb * ntx);
-    const int b = rem / ntx, tx = rem - b * ntx;
-    const uint32_t M = frame_max[f];
-    const uint32_t L = M >= (uint32_t)(kWin - 1) ? M - (kWin - 1) : 0u;
-    if (blk_max[it] < L) continue;  // warp-uniform: nothing in the window here
-    for (int k = lane; k < kBandH * kWin; k += 32) c[k] = 0;
-    __syncwarp();
-    const int y0 = b * kBandH, x0 = tx * kBandW;
-    const int rows = min(kBandH, H - y0), cols = min(kBandW, W - x0);
-    const uint8_t* base = dark + (int64_t)f * dark_fs + (int64_t)y0 * W + x0;
-    for (int r = 0; r < rows; ++r) {
-      const uint8_t* row = base + (int64_t)r * W;
-      if (VEC) {
-        const int x = 16 * lane;
-        if (x < cols) {
-          const uint4 v = __ldcg(reinterpret_cast<const uint4*>(row + x));
-          const uint32_t mx = max3u(max3u(unpack_lo(v.x), unpack_hi(v.x), unpack_lo(v.y)),
-                                    max3u(unpack_hi(v.y), unpack_lo(v.z), unpack_hi(v.z)),
-                                    max2(unpack_lo(v.w), unpack_hi(v.w)));
-          if (max(mx & 0xFFFFu, mx >> 16) >= L) {
-            const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+__device__ __forceinline__ void level_hist_unit(const uint8_t* __restrict__ dark, int64_t dark_fs, int H, int W,
+                                                int f, int b, int u, uint32_t M, uint32_t* c,
+                                                uint32_t* __restrict__ row_hist, uint32_t* __restrict__ frame_hist,
+                                                int lane) {
+  const uint32_t L = M >= (uint32_t)(kWin - 1) ? M - (kWin - 1) : 0u;
+  const int y0 = b * kBandH, x0 = u * kUnitW;
+  const uint8_t* base = dark + (int64_t)f * dark_fs + (int64_t)y0 * W + x0;
+  if (VEC) {  // lane: row lane/2, 16 columns (W % 16 == 0: all in or all out)
+    const int r = lane >> 1, x = 16 * (lane & 1);
+    if (y0 + r < H && x0 + x < W) {
+      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(base + (int64_t)r * W + x));
+      const uint32_t m4 = vmax4(vmax4(v.x, v.y), vmax4(v.z, v.w));
+      const uint32_t mx = max(max(m4 & 0xFFu, (m4 >> 8) & 0xFFu), max((m4 >> 16) & 0xFFu, m4 >> 24));
+      if (mx >= L) {
+        const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const uint32_t bv = (ws[q >> 2] >> (8 * (q & 3))) & 0xFFu;
-              if (bv >= L) atomicAdd(&c[r * kWin + (M - bv)], 1u);
-            }
-          }
-        }
-      } else {
-        for (int x = lane; x < cols; x += 32) {
-          const uint32_t bv = row[x];
+        for (int q = 0; q < 16; ++q) {
+          const uint32_t bv = (ws[q >> 2] >> (8 * (q & 3))) & 0xFFu;
           if (bv >= L) atomicAdd(&c[r * kWin + (M - bv)], 1u);
         }
       }
     }
-    __syncwarp();
-    // flush: per-row entries (rows of this block are shared with other column tiles)
-    uint32_t* rh = row_hist + ((int64_t)f * H + y0) * kWin;
-    for (int k = lane; k < rows * kWin; k += 32) {
-      const uint32_t v = c[k];
-      if (v) atomicAdd(rh + k, v);
+  } else {  // lane: one column, 16 rows
+    const int x = x0 + lane;
+    if (x < W) {
+      const int rows = min(kBandH, H - y0);
+      for (int r = 0; r < rows; ++r) {
+        const uint32_t bv = base[(int64_t)r * W + lane];
+        if (bv >= L) atomicAdd(&c[r * kWin + (M - bv)], 1u);
+      }
     }
-    // per-level totals over the block's rows
-    if (lane < kWin) {
-      uint32_t s = 0;
-      for (int r = 0; r < rows; ++r) s += c[r * kWin + lane];
-      if (s) atomicAdd(frame_hist + (int64_t)f * kWin + lane, s);
+  }
+  __syncwarp();
+  if (lane < kWin) {  // per-level totals over the unit's rows
+    uint32_t s = 0;
+#pragma unroll
+    for (int r = 0; r < kBandH; ++r) s += c[r * kWin + lane];
+    if (s) atomicAdd(frame_hist + (int64_t)f * kWin + lane, s);
+  }
+  __syncwarp();
+  // per-row entries (a row's units are counted by different warps); rows past H hold zeros
+  uint32_t* rh = row_hist + ((int64_t)f * H + y0) * kWin;
+#pragma unroll
+  for (int k = lane; k < kBandH * kWin; k += 32) {
+    const uint32_t v = c[k];
+    if (v) {
+      atomicAdd(rh + k, v);
+      c[k] = 0;
     }
-    __syncwarp();
+  }
+  __syncwarp();
+}
+
+// K2: units are dealt to warps 32 at a time, strided by the number of warps so that
+// each warp's share mixes frames and bands; every lane tests one unit against its
+// frame's window (one gather for 32 units) and the warp then counts the ballot's units.
+template <bool VEC>
+__global__ void __launch_bounds__(kT)
+k_level_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int n, int H, int W,
+             const uint32_t* __restrict__ frame_max, const uint32_t* __restrict__ unit_max,
+             uint32_t* __restrict__ row_hist /* [n][H][16] */, uint32_t* __restrict__ frame_hist /* [n][16] */) {
+  __shared__ uint32_t cnt[kWarps][kBandH * kWin];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nb = (H + kBandH - 1) / kBandH, nu = (W + kUnitW - 1) / kUnitW;
+  const int64_t per_frame = (int64_t)nb * nu, items = (int64_t)n * per_frame;
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  uint32_t* c = cnt[wid];
+  for (int k = lane; k < kBandH * kWin; k += 32) c[k] = 0;
+  __syncwarp();
+  for (int64_t base = (int64_t)blockIdx.x * kWarps + wid; base < items; base += 32 * nw) {
+    const int64_t mine = base + nw * lane;
+    bool want = false;
+    uint32_t M = 0;
+    if (mine < items) {
+      M = frame_max[mine / per_frame];
+      want = unit_max[mine] >= (M >= (uint32_t)(kWin - 1) ? M - (kWin - 1) : 0u);
+    }
+    for (uint32_t mask = __ballot_sync(0xffffffffu, want); mask; mask &= mask - 1) {
+      const int src = __ffs(mask) - 1;
+      const int64_t it = base + nw * src;
+      const int f = (int)(it / per_frame);
+      const int rem = (int)(it - (int64_t)f * per_frame);
+      const int b = rem / nu;
+      level_hist_unit<VEC>(dark, dark_fs, H, W, f, b, rem - b * nu, __shfl_sync(0xffffffffu, M, src), c, row_hist,
+                           frame_hist, lane);
+    }
   }
 }
 
@@ -142,192 +159,214 @@ __device__ void scan_rows(int H, uint32_t* info, Get get) {
 __global__ void __launch_bounds__(kT)
 k_threshold(int64_t npx, int64_t K, int H, const uint32_t* __restrict__ frame_max,
             const uint32_t* __restrict__ row_hist, const uint32_t* __restrict__ frame_hist,
-            FrameSel* __restrict__ sel, uint32_t* __restrict__ row_info) {
+            FrameSel* __restrict__ sel, uint32_t* __restrict__ full_list, uint32_t* __restrict__ row_info) {
   const int f = blockIdx.x;
   __shared__ int js_s;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // warp 0: inclusive scan of the kWin level counts from the top
+    const int lane = threadIdx.x;
     const uint32_t M = frame_max[f];
-    uint32_t mode = kSelFast;
-    int js = -1;
-    uint64_t cum = 0;
-    if (K >= npx) {
-      mode = kSelAll;
-    } else {
-      for (int j = 0; j < kWin && (uint32_t)j <= M; ++j) {
-        const uint32_t h = frame_hist[(int64_t)f * kWin + j];
-        if (cum + h >= (uint64_t)K) { js = j; break; }
-        cum += h;
+    const uint64_t h = (lane < kWin && (uint32_t)lane <= M) ? frame_hist[(int64_t)f * kWin + lane] : 0u;
+    uint64_t inc = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const bool hit = K < npx && lane < kWin && (uint32_t)lane <= M && inc >= (uint64_t)K;
+    const uint32_t hits = __ballot_sync(0xffffffffu, hit);
+    const int js = hits ? __ffs(hits) - 1 : -1;
+    const uint64_t cum = __shfl_sync(0xffffffffu, inc - h, js < 0 ? 0 : js);
+    if (lane == 0) {
+      const uint32_t mode = K >= npx ? kSelAll : (js < 0 ? kSelFull : kSelFast);
+      sel[f].mode = mode;
+      if (mode == kSelFull) full_list[1 + atomicAdd(full_list, 1u)] = (uint32_t)f;
+      if (mode == kSelFast) {
+        sel[f].T = M - js;
+        sel[f].above = (uint32_t)cum;
       }
-      if (js < 0) mode = kSelFull;
+      js_s = mode == kSelFast ? js : -1;
     }
-    sel[f].mode = mode;
-    if (mode == kSelFast) {
-      sel[f].T = M - js;
-      sel[f].above = (uint32_t)cum;
-    }
-    js_s = mode == kSelFast ? js : -1;
   }
   __syncthreads();
   const int js = js_s;
   if (js < 0) return;
   const uint32_t* rh = row_hist + (int64_t)f * H * kWin;
   scan_rows(H, row_info + (int64_t)f * H * 4, [&](int y, uint32_t& a, uint32_t& t) {
-    const uint32_t* h = rh + (int64_t)y * kWin;
-    uint32_t acc = 0;
-    for (int j = 0; j < js; ++j) acc += h[j];
+    const uint4* h4 = reinterpret_cast<const uint4*>(rh + (int64_t)y * kWin);
+    uint32_t h[kWin];
+#pragma unroll
+    for (int q = 0; q < kWin / 4; ++q) {
+      const uint4 v = h4[q];
+      h[4 * q] = v.x; h[4 * q + 1] = v.y; h[4 * q + 2] = v.z; h[4 * q + 3] = v.w;
+    }
+    uint32_t acc = 0, tie = 0;
+#pragma unroll
+    for (int j = 0; j < kWin; ++j) {
+      acc += j < js ? h[j] : 0u;
+      tie = j == js ? h[j] : tie;
+    }
     a = acc;
-    t = h[js];
+    t = tie;
   });
 }
 
 // Fallback for frames whose top K spans more than kWin levels below the max
-// (sel.mode == kSelFull): a full 256-level histogram and per-row counts, each
-// spread over kFullParts CTAs per frame (frames on the fast path exit at once).
+// (sel.mode == kSelFull, listed by K3 in full_list = {count, frames...}): a full
+// 256-level histogram and per-row counts, each spread over kFullParts CTAs per
+// frame.  The grid is (kFullParts, <= kFullFrames); with no listed frame every CTA
+// exits after one load.
 constexpr int kFullParts = 32;
+constexpr int kFullFrames = 16;
 
 // F1: 256-level histogram of the frame's dark bytes (warp-private shared copies);
 // the frame's last CTA to finish (ticket) derives T and the count above it.
 template <bool VEC>
 __global__ void __launch_bounds__(kT)
 k_full_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_t K, FrameSel* __restrict__ sel,
-            uint32_t* __restrict__ hist256) {
-  const int f = blockIdx.y, part = blockIdx.x;
-  if (sel[f].mode != kSelFull) return;
+            const uint32_t* __restrict__ full_list, uint32_t* __restrict__ hist256) {
+  const uint32_t count = __ldcg(full_list);
   __shared__ uint32_t h[kWarps][256];
   __shared__ bool last;
-  const int wid = threadIdx.x >> 5;
-  for (int k = threadIdx.x; k < kWarps * 256; k += kT) (&h[0][0])[k] = 0;
-  __syncthreads();
-  const uint8_t* p = dark + f * dark_fs;
-  uint32_t* hw = h[wid];
-  if (VEC) {
-    const int64_t U = npx / 16, u0 = U * part / kFullParts, u1 = U * (part + 1) / kFullParts;
-    for (int64_t u = u0 + threadIdx.x; u < u1; u += kT) {
-      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(p) + u);
-      const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+  const int wid = threadIdx.x >> 5, part = blockIdx.x;
+  for (uint32_t i = blockIdx.y; i < count; i += gridDim.y) {
+    const int f = (int)__ldcg(full_list + 1 + i);
+    for (int k = threadIdx.x; k < kWarps * 256; k += kT) (&h[0][0])[k] = 0;
+    __syncthreads();
+    const uint8_t* p = dark + f * dark_fs;
+    uint32_t* hw = h[wid];
+    if (VEC) {
+      const int64_t U = npx / 16, u0 = U * part / kFullParts, u1 = U * (part + 1) / kFullParts;
+      for (int64_t u = u0 + threadIdx.x; u < u1; u += kT) {
+        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(p) + u);
+        const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int q = 0; q < 16; ++q) atomicAdd(&hw[(ws[q >> 2] >> (8 * (q & 3))) & 0xFFu], 1u);
+        for (int q = 0; q < 16; ++q) atomicAdd(&hw[(ws[q >> 2] >> (8 * (q & 3))) & 0xFFu], 1u);
+      }
+    } else {
+      const int64_t q0 = npx * part / kFullParts, q1 = npx * (part + 1) / kFullParts;
+      for (int64_t q = q0 + threadIdx.x; q < q1; q += kT) atomicAdd(&hw[p[q]], 1u);
     }
-  } else {
-    const int64_t q0 = npx * part / kFullParts, q1 = npx * (part + 1) / kFullParts;
-    for (int64_t q = q0 + threadIdx.x; q < q1; q += kT) atomicAdd(&hw[p[q]], 1u);
-  }
-  __syncthreads();
-  uint32_t* fh = hist256 + (int64_t)f * 256;
-  for (int b = threadIdx.x; b < 256; b += kT) {
-    uint32_t c = 0;
-    for (int w = 0; w < kWarps; ++w) c += h[w][b];
-    if (c) atomicAdd(fh + b, c);
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&sel[f].ticket, 1u) == kFullParts - 1;
-  __syncthreads();
-  if (!last || threadIdx.x != 0) return;
-  __threadfence();
-  uint64_t cum = 0;
-  int T = 0;
-  for (int v = 255; v >= 0; --v) {
-    const uint32_t c = __ldcg(fh + v);
-    if (cum + c >= (uint64_t)K) {
-      T = v;
-      break;
+    __syncthreads();
+    uint32_t* fh = hist256 + (int64_t)f * 256;
+    for (int b = threadIdx.x; b < 256; b += kT) {
+      uint32_t c = 0;
+      for (int w = 0; w < kWarps; ++w) c += h[w][b];
+      if (c) atomicAdd(fh + b, c);
     }
-    cum += c;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&sel[f].ticket, 1u) == kFullParts - 1;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      __threadfence();
+      uint64_t cum = 0;
+      int T = 0;
+      for (int v = 255; v >= 0; --v) {
+        const uint32_t c = __ldcg(fh + v);
+        if (cum + c >= (uint64_t)K) {
+          T = v;
+          break;
+        }
+        cum += c;
+      }
+      sel[f].T = (uint32_t)T;
+      sel[f].above = (uint32_t)cum;
+    }
   }
-  sel[f].T = (uint32_t)T;
-  sel[f].above = (uint32_t)cum;
 }
 
 // F2: per-row (above, tie) counts, warp per row, rows spread over kFullParts CTAs; the
 // frame's last CTA writes the exclusive prefixes and moves the frame to the fast path.
 __global__ void __launch_bounds__(kT)
 k_full_rows(const uint8_t* __restrict__ dark, int64_t dark_fs, int H, int W, FrameSel* __restrict__ sel,
-            uint32_t* __restrict__ row_info) {
-  const int f = blockIdx.y, part = blockIdx.x;
-  if (sel[f].mode != kSelFull) return;
+            const uint32_t* __restrict__ full_list, uint32_t* __restrict__ row_info) {
+  const uint32_t count = __ldcg(full_list);
   __shared__ bool last;
-  const uint32_t T = __ldcg(&sel[f].T);
-  const uint8_t* p = dark + f * dark_fs;
-  uint4* info = reinterpret_cast<uint4*>(row_info + (int64_t)f * H * 4);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int y = part * kWarps + wid; y < H; y += kWarps * kFullParts) {
-    uint32_t na = 0, nt = 0;
-    for (int x = lane; x < W; x += 32) {
-      const uint32_t b = p[(int64_t)y * W + x];
-      na += b > T;
-      nt += b == T;
-    }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, part = blockIdx.x;
+  for (uint32_t i = blockIdx.y; i < count; i += gridDim.y) {
+    const int f = (int)__ldcg(full_list + 1 + i);
+    const uint32_t T = __ldcg(&sel[f].T);
+    const uint8_t* p = dark + f * dark_fs;
+    uint4* info = reinterpret_cast<uint4*>(row_info + (int64_t)f * H * 4);
+    for (int y = part * kWarps + wid; y < H; y += kWarps * kFullParts) {
+      uint32_t na = 0, nt = 0;
+      for (int x = lane; x < W; x += 32) {
+        const uint32_t b = p[(int64_t)y * W + x];
+        na += b > T;
+        nt += b == T;
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      na += __shfl_xor_sync(0xffffffffu, na, o);
-      nt += __shfl_xor_sync(0xffffffffu, nt, o);
+      for (int o = 16; o > 0; o >>= 1) {
+        na += __shfl_xor_sync(0xffffffffu, na, o);
+        nt += __shfl_xor_sync(0xffffffffu, nt, o);
+      }
+      if (lane == 0) info[y] = make_uint4(na, nt, 0u, 0u);
     }
-    if (lane == 0) info[y] = make_uint4(na, nt, 0u, 0u);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&sel[f].ticket2, 1u) == kFullParts - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      scan_rows(H, row_info + (int64_t)f * H * 4, [&](int y, uint32_t& a, uint32_t& t) {
+        const uint4 v = __ldcg(info + y);
+        a = v.x;
+        t = v.y;
+      });
+      __syncthreads();
+      if (threadIdx.x == 0) sel[f].mode = kSelFast;
+    }
+    __syncthreads();
   }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&sel[f].ticket2, 1u) == kFullParts - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  scan_rows(H, row_info + (int64_t)f * H * 4, [&](int y, uint32_t& a, uint32_t& t) {
-    const uint4 v = __ldcg(info + y);
-    a = v.x;
-    t = v.y;
-  });
-  __syncthreads();
-  if (threadIdx.x == 0) sel[f].mode = kSelFast;
 }
 
 // ---------------------------------------------------------------------------
 // K4: ordered compaction of the rows holding selected pixels + sequential sum
 // ---------------------------------------------------------------------------
-template <bool VEC>
-__device__ void compact_row(const uint8_t* __restrict__ row, int W, uint32_t base_idx, uint32_t T, uint32_t above,
-                            uint32_t need, uint32_t ao, uint32_t to, uint32_t* __restrict__ out, int lane) {
-  for (int x0 = 0; x0 < W; x0 += 512) {
-    uint32_t w[4] = {0u, 0u, 0u, 0u};
-    const int x = x0 + 16 * lane;
-    int nv = 0;
-    if (VEC) {
-      if (x < W) {
-        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(row + x));
-        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
-        nv = 16;
+// One row: only its 32-column units whose maximum reaches T can hold selected pixels.
+// Lane l owns column 32u + l of each such unit, so each unit is one coalesced 32-byte
+// read and its above/tie pixels are placed by ballot + popc in index order.  Up to 8
+// units' loads are in flight together.
+__device__ void compact_row(const uint8_t* __restrict__ row, const uint32_t* __restrict__ um, int nu, int W,
+                            uint32_t base_idx, uint32_t T, uint32_t above, uint32_t need, uint32_t ao, uint32_t to,
+                            uint32_t* __restrict__ out, int lane) {
+  constexpr int kU = 8;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int u0 = 0; u0 < nu; u0 += 32) {
+    const int um_i = u0 + lane;
+    uint32_t hot = __ballot_sync(0xffffffffu, um_i < nu && __ldcg(um + um_i) >= T);
+    while (hot) {
+      int us[kU];
+      int cnt = 0;
+#pragma unroll
+      for (int k = 0; k < kU; ++k) {
+        us[k] = hot ? u0 + __ffs(hot) - 1 : -1;
+        cnt += hot != 0;
+        hot &= hot - 1;
       }
-    } else {
-      nv = max(0, min(16, W - x));
+      uint32_t bv[kU];
 #pragma unroll
-      for (int q = 0; q < 16; ++q)
-        if (q < nv) w[q >> 2] |= (uint32_t)row[x + q] << (8 * (q & 3));
-    }
-    uint32_t na = 0, nt = 0;
+      for (int k = 0; k < kU; ++k) {
+        const int x = kUnitW * us[k] + lane;
+        bv[k] = (us[k] >= 0 && x < W) ? (uint32_t)__ldcg(row + x) : 0u;
+      }
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const uint32_t b = (w[q >> 2] >> (8 * (q & 3))) & 0xFFu;
-      na += (q < nv) && (b > T);
-      nt += (q < nv) && (b == T);
-    }
-    uint32_t ta, tt;
-    uint32_t pa = warp_excl_scan(na, lane, &ta);
-    uint32_t pt = warp_excl_scan(nt, lane, &tt);
-    if (na | nt) {
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const uint32_t b = (w[q >> 2] >> (8 * (q & 3))) & 0xFFu;
-        if (q < nv) {
-          if (b > T) {
-            out[ao + pa++] = base_idx + x + q;
-          } else if (b == T) {
-            const uint32_t r = to + pt++;
-            if (r < need) out[above + r] = base_idx + x + q;
-          }
+      for (int k = 0; k < kU; ++k) {
+        if (k >= cnt) break;  // warp-uniform
+        const int x = kUnitW * us[k] + lane;
+        const bool ok = x < W;
+        const uint32_t am = __ballot_sync(0xffffffffu, ok && bv[k] > T);
+        const uint32_t tm = __ballot_sync(0xffffffffu, ok && bv[k] == T);
+        if (ok && bv[k] > T) {
+          out[ao + __popc(am & lt)] = base_idx + x;
+        } else if (ok && bv[k] == T) {
+          const uint32_t r = to + __popc(tm & lt);
+          if (r < need) out[above + r] = base_idx + x;
         }
+        ao += __popc(am);
+        to += __popc(tm);
       }
     }
-    ao += ta;
-    to += tt;
   }
 }
 
@@ -379,10 +418,10 @@ __device__ void airlight_sum(const uint8_t* __restrict__ frame, const uint32_t* 
 // Warp per row; a frame's rows are spread over kCompactParts CTAs.
 constexpr int kCompactParts = 8;
 
-template <bool VEC>
 __global__ void __launch_bounds__(kT)
 k_compact(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_t K, int H, int W,
-          const FrameSel* __restrict__ sel, const uint32_t* __restrict__ row_info, uint32_t* __restrict__ sel_idx) {
+          const FrameSel* __restrict__ sel, const uint32_t* __restrict__ row_info,
+          const uint32_t* __restrict__ unit_max, uint32_t* __restrict__ sel_idx) {
   const int f = blockIdx.y, part = blockIdx.x;
   const uint32_t mode = sel[f].mode;
   uint32_t* out = sel_idx + (int64_t)f * K;
@@ -396,10 +435,23 @@ k_compact(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_
   const uint32_t need = (uint32_t)K - above;
   const uint4* info = reinterpret_cast<const uint4*>(row_info + (int64_t)f * H * 4);
   const uint8_t* p = dark + f * dark_fs;
-  for (int y = part * kWarps + wid; y < H; y += kWarps * kCompactParts) {
-    const uint4 ri = info[y];  // above, ties, above_prefix, tie_prefix
-    if (ri.x == 0 && (ri.y == 0 || ri.w >= need)) continue;
-    compact_row<VEC>(p + (int64_t)y * W, W, (uint32_t)((int64_t)y * W), T, above, need, ri.z, ri.w, out, lane);
+  const int nb = (H + kBandH - 1) / kBandH, nu = (W + kUnitW - 1) / kUnitW;
+  const uint32_t* fum = unit_max + (int64_t)f * nb * nu;
+  // the warp's rows are y0, y0 + S, y0 + 2S, ...: each lane tests one of 32 of them,
+  // then the warp compacts the rows the ballot marks, in order
+  constexpr int S = kWarps * kCompactParts;
+  for (int y0 = part * kWarps + wid; y0 < H; y0 += 32 * S) {
+    const int ym = y0 + S * lane;
+    uint4 ri = make_uint4(0u, 0u, 0u, 0u);  // above, ties, above_prefix, tie_prefix
+    if (ym < H) ri = info[ym];
+    const bool want = ri.x != 0 || (ri.y != 0 && ri.w < need);
+    for (uint32_t mask = __ballot_sync(0xffffffffu, want); mask; mask &= mask - 1) {
+      const int src = __ffs(mask) - 1;
+      const int y = y0 + S * src;
+      const uint32_t pa = __shfl_sync(0xffffffffu, ri.z, src), pt = __shfl_sync(0xffffffffu, ri.w, src);
+      compact_row(p + (int64_t)y * W, fum + (int64_t)(y / kBandH) * nu, nu, W, (uint32_t)((int64_t)y * W), T,
+                  above, need, pa, pt, out, lane);
+    }
   }
 }
 
@@ -418,28 +470,26 @@ cudaError_t select_u8(const uint8_t* dark, int64_t dark_fs, const uint8_t* in, i
                       int64_t K, double alpha, const SelectWs& ws, double* airlight, cudaStream_t st) {
   const int H = ws.H, W = ws.W;
   const bool vec = (W % 16 == 0) && (dark_fs % 16 == 0) && ((uintptr_t)dark % 16 == 0);
-  const int nb = (H + kBandH - 1) / kBandH, ntx = (W + kBandW - 1) / kBandW;
-  const int64_t items = (int64_t)n * nb * ntx;
+  const int nb = (H + kBandH - 1) / kBandH, nu = (W + kUnitW - 1) / kUnitW;
+  const int64_t items = (int64_t)n * nb * nu;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int g2 = (int)std::min<int64_t>((items + kWarps - 1) / kWarps, 8LL * sms);
+  const int g2 = (int)std::min<int64_t>((items + 32 * kWarps - 1) / (32 * kWarps), 8LL * sms);
   if (vec) {
-    k_level_hist<true><<<g2, kT, 0, st>>>(dark, dark_fs, n, H, W, ws.frame_max, ws.blk_max, ws.row_hist,
+    k_level_hist<true><<<g2, kT, 0, st>>>(dark, dark_fs, n, H, W, ws.frame_max, ws.unit_max, ws.row_hist,
                                           ws.frame_hist);
   } else {
-    k_level_hist<false><<<g2, kT, 0, st>>>(dark, dark_fs, n, H, W, ws.frame_max, ws.blk_max, ws.row_hist,
+    k_level_hist<false><<<g2, kT, 0, st>>>(dark, dark_fs, n, H, W, ws.frame_max, ws.unit_max, ws.row_hist,
                                            ws.frame_hist);
   }
-  k_threshold<<<n, kT, 0, st>>>(npx, K, H, ws.frame_max, ws.row_hist, ws.frame_hist, ws.sel, ws.row_info);
-  const dim3 cgrid(kCompactParts, n), fgrid(kFullParts, n);
-  if (vec) k_full_hist<true><<<fgrid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.sel, ws.hist256);
-  else k_full_hist<false><<<fgrid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.sel, ws.hist256);
-  k_full_rows<<<fgrid, kT, 0, st>>>(dark, dark_fs, H, W, ws.sel, ws.row_info);
-  if (vec)
-    k_compact<true><<<cgrid, kT, 0, st>>>(dark, dark_fs, npx, K, H, W, ws.sel, ws.row_info, ws.sel_idx);
-  else
-    k_compact<false><<<cgrid, kT, 0, st>>>(dark, dark_fs, npx, K, H, W, ws.sel, ws.row_info, ws.sel_idx);
+  k_threshold<<<n, kT, 0, st>>>(npx, K, H, ws.frame_max, ws.row_hist, ws.frame_hist, ws.sel, ws.full_list,
+                                ws.row_info);
+  const dim3 cgrid(kCompactParts, n), fgrid(kFullParts, std::min(n, kFullFrames));
+  if (vec) k_full_hist<true><<<fgrid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.sel, ws.full_list, ws.hist256);
+  else k_full_hist<false><<<fgrid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.sel, ws.full_list, ws.hist256);
+  k_full_rows<<<fgrid, kT, 0, st>>>(dark, dark_fs, H, W, ws.sel, ws.full_list, ws.row_info);
+  k_compact<<<cgrid, kT, 0, st>>>(dark, dark_fs, npx, K, H, W, ws.sel, ws.row_info, ws.unit_max, ws.sel_idx);
   k_airlight<<<n, kT, 0, st>>>(in, in_fs, K, alpha, ws.sel, ws.sel_idx, airlight);
   return cudaGetLastError();
 }
