@@ -245,6 +245,12 @@ __device__ __forceinline__ void pow_tables_init(PowTables& T) {
   }
 }
 
+// Exact u32 -> f64 on the fp64 pipe (2^52 + v has v in its low mantissa bits):
+// keeps int->double conversions off the XU pipe in the hot loops.
+__device__ __forceinline__ double u32_to_f64(uint32_t v) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)v), 4503599627370496.0);
+}
+
 __device__ __forceinline__ double pow_tab(double x, double e, const PowTables& T) {
   if (!(x >= 0x1p-1000)) return 0.0;  // (recovered values are 0 or far above this)
   if (x >= 1.0) return 1.0;
@@ -257,15 +263,19 @@ __device__ __forceinline__ double pow_tab(double x, double e, const PowTables& T
   p = fma(p, eps, -1.0 / 6); p = fma(p, eps, 1.0 / 5); p = fma(p, eps, -1.0 / 4);
   p = fma(p, eps, 1.0 / 3);  p = fma(p, eps, -0.5);    p = fma(p, eps, 1.0);
   constexpr double kLn2Hi = 6.93147180369123816490e-01, kLn2Lo = 1.90821492927058770002e-10;
-  const double y = e * fma((double)ex, kLn2Hi, fma((double)ex, kLn2Lo, T.lnc[j] + p * eps));  // e ln x <= 0
+  const double exd = __dsub_rn(u32_to_f64((uint32_t)(ex + 2048)), 2048.0);  // (double)ex, off the XU pipe
+  const double y = e * fma(exd, kLn2Hi, fma(exd, kLn2Lo, T.lnc[j] + p * eps));  // e ln x <= 0
   if (y < -700.0) return 0.0;
   constexpr double kL64Hi = 0x1.62e42fefa0000p-7, kL64Lo = 2.572804622327669e-14;  // ln2/64 = hi + lo
-  const double k = rint(y * 92.332482616893656);                                     // 64 / ln2
+  // k = rint(y * 64/ln2) and its int by the 1.5 * 2^52 trick (round to nearest even,
+  // like rint; no XU conversions)
+  const double kt = __dadd_rn(__dmul_rn(y, 92.332482616893656), 6755399441055744.0);
+  const double k = __dsub_rn(kt, 6755399441055744.0);
   const double r = fma(-k, kL64Lo, fma(-k, kL64Hi, y));
   double q = 1.0 / 720;
   q = fma(q, r, 1.0 / 120); q = fma(q, r, 1.0 / 24); q = fma(q, r, 1.0 / 6);
   q = fma(q, r, 0.5);       q = fma(q, r, 1.0);      q = fma(q, r, 1.0);
-  const int ki = (int)k;
+  const int ki = __double2loint(kt);
   return q * T.e2[ki & 63] * __longlong_as_double((long long)((ki >> 6) + 1023) << 52);
 }
 

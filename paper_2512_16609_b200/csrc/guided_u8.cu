@@ -57,7 +57,8 @@ __device__ __forceinline__ double guide_t(const GuideTables& T, uint32_t r, uint
 __device__ __forceinline__ double guide_arith(uint32_t r, uint32_t g, uint32_t b) {
   constexpr double k255 = 255.0;
   constexpr double rk = 0x1.0101010101010p-8;  // RN(1/255)
-  const double xr = div_rb((double)r, k255, rk), xg = div_rb((double)g, k255, rk), xb = div_rb((double)b, k255, rk);
+  const double xr = div_rb(u32_to_f64(r), k255, rk), xg = div_rb(u32_to_f64(g), k255, rk),
+               xb = div_rb(u32_to_f64(b), k255, rk);
   const double v = __dadd_rn(__dadd_rn(__dmul_rn(0.299, xr), __dmul_rn(0.587, xg)), __dmul_rn(0.114, xb));
   return fmin(v, 1.0);  // v >= 0
 }

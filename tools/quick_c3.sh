@@ -3,9 +3,9 @@
 # line (stage times), and the ncu launch list of the bench command.
 mkdir -p gpurun_out
 make -C paper_2512_16609_b200/csrc -j16 > /dev/null 2>&1 || { echo build failed; exit 1; }
-timeout 900 python -m pytest tests/test_video_gpu.py tests/test_fullsize_gpu.py tests/test_golden_gpu.py -x -q > gpurun_out/pt.log 2>&1
+timeout 900 python -m pytest ${TESTS:-tests/test_video_gpu.py tests/test_fullsize_gpu.py tests/test_golden_gpu.py} -x -q > gpurun_out/pt.log 2>&1
 tail -2 gpurun_out/pt.log
-python bench.py --no-cpu-baseline --e2e-steps 0 --steps 20 ${BENCH_ARGS} > gpurun_out/bench_q.json 2> gpurun_out/bench_q.err
+python bench.py --no-cpu-baseline --e2e-steps 0 --steps ${STEPS:-20} ${BENCH_ARGS} > gpurun_out/bench_q.json 2> gpurun_out/bench_q.err
 python - <<'PY'
 import json
 d = json.loads(open("gpurun_out/bench_q.json").read().strip().splitlines()[-1])
