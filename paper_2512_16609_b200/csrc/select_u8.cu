@@ -136,7 +136,7 @@ k_level_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int n, int H, in
 template <typename Get>
 __device__ void scan_rows(int H, uint32_t* info, Get get) {
   __shared__ uint32_t tmp[32];
-  const int cpt = (H + kT - 1) / kT;
+  const int cpt = (H + (int)blockDim.x - 1) / (int)blockDim.x;
   const int y0 = threadIdx.x * cpt, y1 = min(H, y0 + cpt);
   uint32_t la = 0, lt = 0;
   for (int y = y0; y < y1; ++y) {
@@ -374,16 +374,27 @@ __device__ void compact_row(const uint8_t* __restrict__ row, const uint32_t* __r
 // (lanes 0..2 of warp 0), so large K is bound by the three dependent fp64 chains.
 __device__ void airlight_sum(const uint8_t* __restrict__ frame, const uint32_t* __restrict__ idx, int64_t K,
                              bool all, double alpha, double* __restrict__ A) {
-  constexpr int kChunk = 2048;
+  constexpr int kChunk = 512;  // small first gather: the chains start early
   __shared__ double tab[256];
   __shared__ uint32_t buf[2][kChunk];
   for (int v = threadIdx.x; v < 256; v += kT) tab[v] = __ddiv_rn((double)v, 255.0);
   auto gather = [&](int64_t base, uint32_t* dst, int t0, int stride) {
     const int cnt = (int)min((int64_t)kChunk, K - base);
-    for (int e = t0; e < cnt; e += stride) {
-      const int64_t px = all ? base + e : (int64_t)__ldcg(idx + base + e);
-      const uint8_t* q = frame + 3 * px;
-      dst[e] = (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16);
+    // all of a thread's index loads first, then all of its pixel loads (two rounds of
+    // memory latency per chunk instead of two per element)
+    constexpr int kMaxPer = 4;  // kChunk / (kT - 32) rounded up
+    int64_t px[kMaxPer];
+#pragma unroll
+    for (int j = 0; j < kMaxPer; ++j) {
+      const int e = t0 + j * stride;
+      px[j] = e < cnt ? (all ? base + e : (int64_t)__ldcg(idx + base + e)) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxPer; ++j) {
+      if (px[j] >= 0) {
+        const uint8_t* q = frame + 3 * px[j];
+        dst[t0 + j * stride] = (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16);
+      }
     }
   };
   gather(0, buf[0], threadIdx.x, kT);
@@ -398,6 +409,8 @@ __device__ void airlight_sum(const uint8_t* __restrict__ frame, const uint32_t* 
     } else if (threadIdx.x < 3) {  // lanes 0..2 of warp 0: one sequential chain per channel
       const uint32_t* b = buf[cur];
       int e = 0;
+      // unrolled: later groups' shared loads issue ahead of this group's dependent adds
+#pragma unroll 4
       for (; e + 8 <= cnt; e += 8) {
         double v[8];
 #pragma unroll
