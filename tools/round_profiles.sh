@@ -12,7 +12,7 @@ done
 python bench.py --config c5 --steps 3 --e2e-steps 1 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_c3.json 2> gpurun_out/bench_ref.err
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k "regex:k_(dark|level|thresh|compact|airlight|build|recover)" --csv --log-file gpurun_out/launches_c3.csv \
+    -k "regex:k_" --csv --log-file gpurun_out/launches_c3.csv \
     python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 ncu --set full --import-source on --clock-control none -k "regex:k_(dark_rows|recover_lut_diag)" -c 2 \
     -o gpurun_out/full_c3 python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline \
