@@ -42,22 +42,33 @@ struct RowGeo {
   static constexpr size_t SMEM = (size_t)ROWS * kTW;
 };
 
+// Pipe balance.  Both passes are bound by the integer ALU pipe (~90 % busy in ncu,
+// the FMA pipe ~10 %).  A pixel's value sits in the HIGH byte of its 16-bit lane with
+// anything in the low byte: a 16-bit min or max then carries the min/max of the
+// high bytes, so the channel split needs no masking (3 PRMT per pair, no LOP3) and
+// pass 2 unpacks a shared-memory word w as the lane pairs (w << 8, w) — an IMAD.SHL
+// on the FMA pipe and nothing — instead of two PRMTs (K1 0.578 -> 0.538 ms on C3).
+// (Moving the 16-bit lane shifts to the FMA pipe as mad.hi(a, 2^16, b * 2^16)
+// measured slower for every subset of them: 0.551-0.628 ms.)
 template <int NP>
 __device__ __forceinline__ uint32_t at(const uint32_t (&m)[NP], int px) {
   return (px & 1) ? shift1(m[px >> 1], m[(px >> 1) + 1]) : m[px >> 1];
 }
 
-// channel minimum of 16 pixels (48 bytes in 12 words) as 8 16x2 pairs
+// channel minimum of 16 pixels (48 bytes in 12 words) as 8 16x2 pairs, each pixel's
+// value in the high byte of its lane (low byte: another channel's byte)
 __device__ __forceinline__ void cmin16_pairs(const uint32_t (&w)[12], uint32_t (&c)[8]) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const uint32_t a = w[3 * q], b = w[3 * q + 1], d = w[3 * q + 2];
-    c[2 * q] = min3(__byte_perm(a, 0u, 0x4340), __byte_perm(a, b, 0x0401) & 0x00FF00FFu,
-                    __byte_perm(a, b, 0x0502) & 0x00FF00FFu);
-    c[2 * q + 1] = min3(__byte_perm(b, d, 0x0502) & 0x00FF00FFu, __byte_perm(b, d, 0x0603) & 0x00FF00FFu,
-                        __byte_perm(d, 0u, 0x4340));
+    // pixels 4q, 4q+1: R (a0, a3), G (a1, b0), B (a2, b1)
+    c[2 * q] = min3(__byte_perm(a, a, 0x3300), __byte_perm(a, b, 0x4411), __byte_perm(a, b, 0x5522));
+    // pixels 4q+2, 4q+3: R (b2, d1), G (b3, d2), B (d0, d3)
+    c[2 * q + 1] = min3(__byte_perm(b, d, 0x5522), __byte_perm(b, d, 0x6633), __byte_perm(d, d, 0x3300));
   }
 }
+// high bytes of two lane pairs -> 4 bytes [lo.1, lo.3, hi.1, hi.3]
+__device__ __forceinline__ uint32_t pack_hi(uint32_t lo, uint32_t hi) { return __byte_perm(lo, hi, 0x7531); }
 
 template <int L, int N>
 __device__ __forceinline__ void vert_levels(uint32_t (&v)[N]) {
@@ -157,7 +168,7 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
         else if (L <= 2 * P) pr[h] = min2(at(m, s), at(m, s + L - P));
         else pr[h] = min3(at(m, s), at(m, s + P), at(m, s + L - P));
       }
-      o[q] = pack2(pr[0], pr[1]);
+      o[q] = pack_hi(pr[0], pr[1]);
     }
     if (lane >= 1 && lane <= 30)
       *reinterpret_cast<uint4*>(hrow + (size_t)v * kTW + 16 * (lane - 1)) = make_uint4(o[0], o[1], o[2], o[3]);
@@ -180,8 +191,8 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       const uint32_t w = *reinterpret_cast<const uint32_t*>(hrow + (size_t)(j0 + k) * kTW + 4 * g);
-      lo[k] = unpack_lo(w);
-      hi[k] = unpack_hi(w);
+      lo[k] = w << 8;  // pixels 0, 2 in the high bytes
+      hi[k] = w;       // pixels 1, 3
     }
     vert_levels<L, N>(lo);
     vert_levels<L, N>(hi);
@@ -193,7 +204,7 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
 #pragma unroll
         for (int j = 0; j < kRun; ++j) {
           const uint32_t a = vert_final<L, N>(lo, j), b = vert_final<L, N>(hi, j);
-          dst[j * wstep] = pack2(a, b);
+          dst[j * wstep] = __byte_perm(a, b, 0x7351);
           mx = max3u(mx, a, b);
         }
       } else {
@@ -201,13 +212,13 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
         for (int j = 0; j < kRun; ++j) {
           const uint32_t a = vert_final<L, N>(lo, j), b = vert_final<L, N>(hi, j);
           if (y0 + j0 + j < H) {
-            dst[j * wstep] = pack2(a, b);
+            dst[j * wstep] = __byte_perm(a, b, 0x7351);
             mx = max3u(mx, a, b);
           }
         }
       }
     }
-    item_max[it] = max(mx & 0xFFFFu, mx >> 16);
+    item_max[it] = max((mx >> 8) & 0xFFu, mx >> 24);
   }
   __syncthreads();
   // unit maxima (8 column groups of 4 = 32 columns) and the frame maximum
