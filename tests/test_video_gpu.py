@@ -156,3 +156,21 @@ def test_batches_beyond_the_grid_limit(oracle):
         m = {}
         want = oracle.dehaze_frame(frames[i], p, m)
         assert np.array_equal(out[i], want) and np.array_equal(air[i], m["airlight"])
+
+
+@pytest.mark.parametrize("r", list(range(1, 17)))
+def test_k1_tiles_every_radius(oracle, r):
+    """K1's vectorised path (width % 16 == 0, r <= 16) across tile seams: 130 rows
+    (three 64-row tile rows, the last partial), 976 columns (three 480-column tiles,
+    the last partial); plateaus, extreme values and noise so every lane of the
+    16-bit pairs sees 0, 255 and ties."""
+    rng = np.random.default_rng(500 + r)
+    H, W = 130, 976
+    f0 = rng.integers(0, 256, size=(H, W, 3), dtype=np.uint8)
+    f1 = np.full((H, W, 3), 200, dtype=np.uint8)
+    f1[40:90, 470:500] = 255  # plateau across a tile seam
+    f1[::7, ::11] = 0        # isolated minima
+    f1[:, 959:] = rng.integers(0, 256, size=(H, W - 959, 3), dtype=np.uint8)
+    f2 = (np.add.outer(np.arange(H), np.arange(W)) % 256).astype(np.uint8)[..., None].repeat(3, axis=2)
+    f2[..., 1] = 255 - f2[..., 1]
+    _check(np.stack([f0, f1, f2]), _params(patch_radius=r), oracle)
