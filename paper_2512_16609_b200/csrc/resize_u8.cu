@@ -138,6 +138,9 @@ k_rs_dark_t(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, double* 
             uint32_t* __restrict__ hist) {
   constexpr int S = 8;                       // outputs per thread and pass
   constexpr int PH = kTH + 2 * R, PW = kTW + 2 * R;
+  // shared-memory pitches (in doubles): odd, so the 32 rows a warp reads in the row
+  // pass (and writes as row minima) fall on 16 distinct 8-byte bank pairs
+  constexpr int PWP = PW | 1, RP = kTW + 1;
   constexpr int kRowItems = PH * (kTW / S);
   constexpr int kRowIter = (kRowItems + kT1 - 1) / kT1;
   constexpr int kHistWords = (kResizeBuckets + 1) / 2;  // 16-bit counters (a tile has <= 2048 outputs)
@@ -146,7 +149,7 @@ k_rs_dark_t(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, double* 
   __shared__ uint32_t s_hist[kHistWords];
   const int f = blockIdx.z;
   const int ty0 = blockIdx.y * kTH, tx0 = blockIdx.x * kTW;
-  double* cm = sm;  // [PH][PW] resized channel minimum (clamped coordinates); then [PH][kTW] row minima
+  double* cm = sm;  // [PH][PWP] resized channel minimum (clamped coordinates); then [PH][RP] row minima
   __shared__ TapS s_ty[PH], s_tx[PW];
   s_f[threadIdx.x] = u8f(threadIdx.x);
   for (int b = threadIdx.x; b < kHistWords; b += kT1) s_hist[b] = 0;
@@ -163,20 +166,21 @@ k_rs_dark_t(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, double* 
     double rgb[3], rgb2[3];
     resized_rgb_t(frame, G.w, expand(s_ty[py], G.h), expand(s_tx[px], G.w), s_f, rgb);
     resized_rgb_t(frame, G.w, expand(s_ty[py2], G.h), expand(s_tx[px2], G.w), s_f, rgb2);
-    cm[e] = fmin(fmin(rgb[0], rgb[1]), rgb[2]);  // estimation.py:38
-    if (e + kT1 < PH * PW) cm[e2] = fmin(fmin(rgb2[0], rgb2[1]), rgb2[2]);
+    cm[py * PWP + px] = fmin(fmin(rgb[0], rgb[1]), rgb[2]);  // estimation.py:38
+    if (e + kT1 < PH * PW) cm[py2 * PWP + px2] = fmin(fmin(rgb2[0], rgb2[1]), rgb2[2]);
   }
   __syncthreads();
-  // rows first (morphology.py:73): item = (row, 8-column segment); all of a thread's
-  // windows are reduced into registers before the row minima overwrite cm in place
+  // rows first (morphology.py:73): item = (8-column segment, row), lanes on consecutive
+  // rows; all of a thread's windows are reduced into registers before the row minima
+  // overwrite cm in place
   {
     double o[kRowIter][S];
 #pragma unroll
     for (int k = 0; k < kRowIter; ++k) {
       const int e = threadIdx.x + k * kT1;
       if (e < kRowItems) {
-        const int py = e / (kTW / S), seg = e - py * (kTW / S);
-        const double* row = cm + py * PW + seg * S;
+        const int seg = e / PH, py = e - seg * PH;
+        const double* row = cm + py * PWP + seg * S;
         double v[S + 2 * R];
 #pragma unroll
         for (int i = 0; i < S + 2 * R; ++i) v[i] = row[i];
@@ -188,22 +192,22 @@ k_rs_dark_t(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, double* 
     for (int k = 0; k < kRowIter; ++k) {
       const int e = threadIdx.x + k * kT1;
       if (e < kRowItems) {
-        const int py = e / (kTW / S), seg = e - py * (kTW / S);
+        const int seg = e / PH, py = e - seg * PH;
 #pragma unroll
-        for (int i = 0; i < S; ++i) cm[py * kTW + seg * S + i] = o[k][i];
+        for (int i = 0; i < S; ++i) cm[py * RP + seg * S + i] = o[k][i];
       }
     }
   }
   __syncthreads();
-  const double* rm = cm;  // [PH][kTW]
+  const double* rm = cm;  // [PH][RP]
   // columns: item = (column, 8-row segment); lanes take consecutive columns
   const int64_t npx = (int64_t)G.H * G.W;
   for (int e = threadIdx.x; e < kTW * (kTH / S); e += kT1) {
     const int seg = e / kTW, px = e - seg * kTW;
-    const double* col = rm + seg * S * kTW + px;
+    const double* col = rm + seg * S * RP + px;
     double v[S + 2 * R], o[S];
 #pragma unroll
-    for (int i = 0; i < S + 2 * R; ++i) v[i] = col[i * kTW];
+    for (int i = 0; i < S + 2 * R; ++i) v[i] = col[i * RP];
     window_min<R, S>(v, o);
     const int x = tx0 + px;
 #pragma unroll
@@ -608,7 +612,8 @@ cudaError_t resize_dark(const uint8_t* in, int64_t in_fs, int n, const ResizeGeo
                         uint32_t* hist, cudaStream_t st) {
   if (r < 1 || r > kResizeMaxRadius) return cudaErrorInvalidValue;
   const size_t smem = (size_t)((kTH + 2 * r) * (kTW + 2 * r) + (kTH + 2 * r) * kTW) * sizeof(double);
-  const size_t smem_t = (size_t)(kTH + 2 * r) * (kTW + 2 * r) * sizeof(double);  // row minima in place
+  // row minima in place; odd pitch (k_rs_dark_t PWP)
+  const size_t smem_t = (size_t)(kTH + 2 * r) * ((kTW + 2 * r) | 1) * sizeof(double);
   dim3 grid((g.W + kTW - 1) / kTW, (g.H + kTH - 1) / kTH, n);
   auto launch = [&](auto kern) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t);
