@@ -102,6 +102,20 @@ __device__ __forceinline__ void thread_offsets(double (&tot)[NQ], double (*wt)[k
   }
 }
 
+// A thread's CPT consecutive prefix values, 16 bytes at a time where CPT allows (the
+// destination is 16-byte aligned: prefix arrays start one double past a 16-byte
+// boundary): per-double stores at a 4-double lane stride hit 4 of the 16 bank pairs.
+template <int CPT>
+__device__ __forceinline__ void store_cols(double* dst, const double (&v)[CPT]) {
+  if (CPT % 2 == 0) {
+#pragma unroll
+    for (int k = 0; k < CPT; k += 2) *reinterpret_cast<double2*>(dst + k) = make_double2(v[k], v[k + 1]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) dst[k] = v[k];
+  }
+}
+
 // ---------------------------------------------------------------- pass 1 ----
 // a, b for every pixel of the strip x in [x0, x0 + 256*CPT - 2r), rows [y0, y0 + seg).
 template <int CPT>
@@ -111,9 +125,9 @@ k_gf_pass1(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
            double* __restrict__ b_out) {
   constexpr int NC = kThreads * CPT;
   __shared__ GuideTables T;
-  extern __shared__ double dyn_pre[];  // [2 buffers][4 sums][NC + 1] prefix rows
+  extern __shared__ __align__(16) double dyn_pre[];  // [2 buffers][4 sums][NC + 2] prefix rows (+1 lead)
   __shared__ double wt[2][4][kThreads / 32];
-  auto pre = [&](int buf, int q) { return dyn_pre + (buf * 4 + q) * (NC + 1); };
+  auto pre = [&](int buf, int q) { return dyn_pre + 1 + (buf * 4 + q) * (NC + 2); };
   const int f = blockIdx.z;
   const int sw = NC - 2 * r;                     // output columns of this strip
   const int x0 = blockIdx.x * sw;                // first output column
@@ -180,12 +194,10 @@ k_gf_pass1(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
     thread_offsets<4>(off, wt[buf]);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      double run = off[q];
+      double run[CPT];
 #pragma unroll
-      for (int k = 0; k < CPT; ++k) {
-        run = __dadd_rn(run, s[q][k]);
-        pre(buf, q)[threadIdx.x * CPT + k + 1] = run;
-      }
+      for (int k = 0; k < CPT; ++k) run[k] = __dadd_rn(k ? run[k - 1] : off[q], s[q][k]);
+      store_cols<CPT>(pre(buf, q) + threadIdx.x * CPT + 1, run);
     }
     __syncthreads();
 #pragma unroll
@@ -226,9 +238,9 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
   __shared__ GuideTables T;  // wr/wg/wb for the guide; t[] holds v/255 here
   __shared__ double sA[3], s_thr[256];
   __shared__ PowTables PT;  // balance sums (MODE 1)
-  extern __shared__ double dyn_pre[];  // [2 buffers][2 sums][NC + 1] prefix rows
+  extern __shared__ __align__(16) double dyn_pre[];  // [2 buffers][2 sums][NC + 2] prefix rows (+1 lead)
   __shared__ double wt[2][2][kThreads / 32];
-  auto pre = [&](int buf, int q) { return dyn_pre + (buf * 2 + q) * (NC + 1); };
+  auto pre = [&](int buf, int q) { return dyn_pre + 1 + (buf * 2 + q) * (NC + 2); };
   const int f = blockIdx.z;
   const int sw = NC - 2 * r;
   const int x0 = blockIdx.x * sw;
@@ -283,14 +295,14 @@ k_gf_pass2(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, int r, i
     }
     thread_offsets<2>(off, wt[buf]);
     {
-      double ra = off[0], rb = off[1];
+      double ra[CPT], rb[CPT];
 #pragma unroll
       for (int k = 0; k < CPT; ++k) {
-        ra = __dadd_rn(ra, sa[k]);
-        rb = __dadd_rn(rb, sb[k]);
-        pre(buf, 0)[threadIdx.x * CPT + k + 1] = ra;
-        pre(buf, 1)[threadIdx.x * CPT + k + 1] = rb;
+        ra[k] = __dadd_rn(k ? ra[k - 1] : off[0], sa[k]);
+        rb[k] = __dadd_rn(k ? rb[k - 1] : off[1], sb[k]);
       }
+      store_cols<CPT>(pre(buf, 0) + threadIdx.x * CPT + 1, ra);
+      store_cols<CPT>(pre(buf, 1) + threadIdx.x * CPT + 1, rb);
     }
     __syncthreads();
 #pragma unroll
@@ -464,7 +476,7 @@ int guided_cpt(int W, int r) {
 }
 
 template <int CPT>
-size_t pass_smem(int nsums) { return (size_t)2 * nsums * (kThreads * CPT + 1) * sizeof(double); }
+size_t pass_smem(int nsums) { return ((size_t)2 * nsums * (kThreads * CPT + 2) + 2) * sizeof(double); }
 
 }  // namespace
 
