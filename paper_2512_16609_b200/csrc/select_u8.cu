@@ -33,6 +33,10 @@ namespace {
 
 constexpr int kT = 256;
 constexpr int kWarps = kT / 32;
+// Row pitch of K2's warp-private (row, level) counters: odd, so the 16 rows of a unit
+// (two lanes per row) counting the same level hit 16 different banks (pitch 16 put
+// every other row on the same bank: 8-way conflicts on the shared atomics).
+constexpr int kCntPitch = kWin + 1;
 
 // ---------------------------------------------------------------------------
 // K2: per-row level histogram of the levels [M-15, M]
@@ -58,7 +62,7 @@ __device__ __forceinline__ void level_hist_unit(const uint8_t* __restrict__ dark
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
           const uint32_t bv = (ws[q >> 2] >> (8 * (q & 3))) & 0xFFu;
-          if (bv >= L) atomicAdd(&c[r * kWin + (M - bv)], 1u);
+          if (bv >= L) atomicAdd(&c[r * kCntPitch + (M - bv)], 1u);
         }
       }
     }
@@ -68,7 +72,7 @@ __device__ __forceinline__ void level_hist_unit(const uint8_t* __restrict__ dark
       const int rows = min(kBandH, H - y0);
       for (int r = 0; r < rows; ++r) {
         const uint32_t bv = base[(int64_t)r * W + lane];
-        if (bv >= L) atomicAdd(&c[r * kWin + (M - bv)], 1u);
+        if (bv >= L) atomicAdd(&c[r * kCntPitch + (M - bv)], 1u);
       }
     }
   }
@@ -76,7 +80,7 @@ __device__ __forceinline__ void level_hist_unit(const uint8_t* __restrict__ dark
   if (lane < kWin) {  // per-level totals over the unit's rows
     uint32_t s = 0;
 #pragma unroll
-    for (int r = 0; r < kBandH; ++r) s += c[r * kWin + lane];
+    for (int r = 0; r < kBandH; ++r) s += c[r * kCntPitch + lane];
     if (s) atomicAdd(frame_hist + (int64_t)f * kWin + lane, s);
   }
   __syncwarp();
@@ -84,10 +88,11 @@ __device__ __forceinline__ void level_hist_unit(const uint8_t* __restrict__ dark
   uint32_t* rh = row_hist + ((int64_t)f * H + y0) * kWin;
 #pragma unroll
   for (int k = lane; k < kBandH * kWin; k += 32) {
-    const uint32_t v = c[k];
+    uint32_t* ck = c + (k / kWin) * kCntPitch + (k % kWin);
+    const uint32_t v = *ck;
     if (v) {
       atomicAdd(rh + k, v);
-      c[k] = 0;
+      *ck = 0;
     }
   }
   __syncwarp();
@@ -101,13 +106,13 @@ __global__ void __launch_bounds__(kT)
 k_level_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int n, int H, int W,
              const uint32_t* __restrict__ frame_max, const uint32_t* __restrict__ unit_max,
              uint32_t* __restrict__ row_hist /* [n][H][16] */, uint32_t* __restrict__ frame_hist /* [n][16] */) {
-  __shared__ uint32_t cnt[kWarps][kBandH * kWin];
+  __shared__ uint32_t cnt[kWarps][kBandH * kCntPitch];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nb = (H + kBandH - 1) / kBandH, nu = (W + kUnitW - 1) / kUnitW;
   const int64_t per_frame = (int64_t)nb * nu, items = (int64_t)n * per_frame;
   const int64_t nw = (int64_t)gridDim.x * kWarps;
   uint32_t* c = cnt[wid];
-  for (int k = lane; k < kBandH * kWin; k += 32) c[k] = 0;
+  for (int k = lane; k < kBandH * kCntPitch; k += 32) c[k] = 0;
   __syncwarp();
   for (int64_t base = (int64_t)blockIdx.x * kWarps + wid; base < items; base += 32 * nw) {
     const int64_t mine = base + nw * lane;
