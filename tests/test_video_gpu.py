@@ -174,3 +174,43 @@ def test_k1_tiles_every_radius(oracle, r):
     f2 = (np.add.outer(np.arange(H), np.arange(W)) % 256).astype(np.uint8)[..., None].repeat(3, axis=2)
     f2[..., 1] = 255 - f2[..., 1]
     _check(np.stack([f0, f1, f2]), _params(patch_radius=r), oracle)
+
+
+def test_balance_out_of_band_samples(oracle):
+    # uniform noise: most non-minimum samples lie >= 64 levels above their pixel's
+    # minimum, outside the banded table (k_balance_band's per-unit correction path)
+    rng = np.random.default_rng(37)
+    frames = rng.integers(0, 256, size=(3, 64, 96, 3), dtype=np.uint8)
+    frames[1, :, :, 0] = 255                      # one saturated channel: d = 255 - m everywhere
+    p = _params(white_balance=True)
+    out, air, _, _ = _run(frames, p)
+    for i, f in enumerate(frames):
+        m = {}
+        want = oracle.dehaze_frame(f, p, m)
+        assert np.array_equal(air[i], m["airlight"])
+        d = np.abs(out[i].astype(np.int16) - want.astype(np.int16))
+        assert d.max() <= 1 and int((d > 0).sum()) <= 2
+
+
+def test_balance_sums_independent_of_kernel_and_batch():
+    # the channel sums are exact integer sums of the quantised g samples, so the
+    # banded kernel (16-byte aligned frames), the scalar kernel (a frame buffer one
+    # byte off alignment) and any batch composition give the same bytes
+    from paper_2512_16609_b200.engine import engine_for
+    from paper_2512_16609_b200.synthetic import make_frames
+
+    dev = torch.device("cuda", 0)
+    frames = make_frames("c4", frames=3, width=160, height=96).to(dev)
+    frames[2] = torch.randint(0, 256, frames[2].shape, dtype=torch.uint8, device=dev, generator=torch.Generator(dev).manual_seed(41))
+    p = _params(white_balance=True)
+    eng = engine_for(dev)
+    aligned, _ = eng.run(frames, p)[:2]
+    raw = torch.empty(frames.numel() + 16, dtype=torch.uint8, device=dev)
+    shifted = raw[1:1 + frames.numel()].view(frames.shape)
+    shifted.copy_(frames)
+    assert shifted.data_ptr() % 16 == 1
+    scalar, _ = eng.run(shifted, p)[:2]
+    single, _ = eng.run(frames[1:2].clone(), p)[:2]
+    torch.cuda.synchronize()
+    assert torch.equal(aligned, scalar)
+    assert torch.equal(aligned[1:2], single)

@@ -17,4 +17,10 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 ncu --set full --import-source on --clock-control none -k "regex:k_(dark_rows|recover_lut_diag)" -c 2 \
     -o gpurun_out/full_c3 python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline \
     > gpurun_out/ncu_full.log 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k "regex:k_" --csv --log-file gpurun_out/launches_c4.csv \
+    python bench.py --config c4 --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_launch_c4.log 2>&1
+ncu --set full --import-source on --clock-control none -k "regex:k_(balance_band|build_g)" -c 2 \
+    -o gpurun_out/full_c4_balance python bench.py --config c4 --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline \
+    > gpurun_out/ncu_full_c4.log 2>&1
 echo done
