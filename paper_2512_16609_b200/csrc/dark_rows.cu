@@ -117,9 +117,9 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
   auto load_row = [&](int v, uint4& a, uint4& b, uint4& d) {
     const int y = y0 - R + v;
     if (v < G::ROWS && y >= 0 && y < H && col_ok) {
-      a = ldg_nc_v4(src_row);
-      b = ldg_nc_v4(src_row + 16);
-      d = ldg_nc_v4(src_row + 32);
+      a = ldg_v4(src_row);
+      b = ldg_v4(src_row + 16);
+      d = ldg_v4(src_row + 32);
     } else {
       a = b = d = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
     }
