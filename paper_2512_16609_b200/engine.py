@@ -26,6 +26,15 @@ def top_k(npx: int, top_fraction: float) -> int:
     return max(1, math.floor(top_fraction * npx))
 
 
+def _check_buffer(t, name, shape, dtype, dev):
+    """Caller-supplied output buffers: the ABI writes through raw pointers."""
+    if not isinstance(t, torch.Tensor) or t.device != dev or t.dtype != dtype or tuple(t.shape) != tuple(shape) \
+            or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous {dtype} tensor of shape {tuple(shape)} on {dev}, got "
+                         f"{tuple(getattr(t, 'shape', ()))} {getattr(t, 'dtype', type(t))} "
+                         f"on {getattr(t, 'device', '?')}")
+
+
 def native_params(params, npx: int, thresholds: torch.Tensor) -> _native.DhzParams:
     p = _native.DhzParams()
     p.mode = 1 if params.mode == "image" else 0
@@ -52,11 +61,47 @@ class FrameEngine:
         self.device = torch.device(device)
         self._ws = None
         self._lock = threading.Lock()
+        # the workspace is reused by every run: a run enqueued on another stream
+        # waits for the previous run's kernels (event recorded after each run)
+        self._last = None  # (cuda stream handle, torch.cuda.Event)
 
     def workspace(self, nbytes: int) -> torch.Tensor:
         if self._ws is None or self._ws.numel() < nbytes:
             self._ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)
         return self._ws
+
+    def _order_after_last(self, st):
+        last = self._last
+        if last is None or last[0] == st.cuda_stream:
+            return
+        if torch.cuda.is_current_stream_capturing():
+            return  # inside a graph capture the caller orders the captured work
+        st.wait_event(last[1])
+
+    def _mark_done(self, st):
+        if torch.cuda.is_current_stream_capturing():
+            self._last = None
+            return
+        ev = torch.cuda.Event()
+        ev.record(st)
+        self._last = (st.cuda_stream, ev)
+
+    def _maps(self, ws, n, h, w, H, W, p, resize, st):
+        """Copies of the dark map and selected indices left in the workspace (on ``st``)."""
+        k = p.top_k
+        with torch.cuda.stream(st):
+            if resize:
+                off = (ctypes.c_int64 * 5)()
+                _native.check(self.lib.dhz_frames_resize_u8_layout(n, h, w, H, W, ctypes.byref(p), off),
+                              "dhz_frames_resize_u8_layout")
+                maps = {"dark_f64": ws[off[0]: off[0] + off[1] * n].view(torch.float64).view(n, H, W).clone()}
+            else:
+                off = self.layout(n, H, W, p)
+                dark_fs = off[1]
+                maps = {"dark_u8": ws[off[0]: off[0] + dark_fs * n].view(n, dark_fs)[:, : H * W]
+                        .reshape(n, H, W).clone()}
+            maps["selected"] = ws[off[2]: off[2] + 4 * n * k].view(torch.int32).view(n, k).clone()
+        return maps
 
     def layout(self, n, H, W, p):
         off = (ctypes.c_int64 * 5)()
@@ -95,8 +140,12 @@ class FrameEngine:
         p = native_params(params, H * W, thr)
         if out is None:
             out = torch.empty((n, H, W, 3), dtype=torch.uint8, device=dev)
+        else:
+            _check_buffer(out, "out", (n, H, W, 3), torch.uint8, dev)
         if airlight is None:
             airlight = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        else:
+            _check_buffer(airlight, "airlight", (n, 3), torch.float64, dev)
         if n == 0:
             return (out, airlight, {}) if keep_maps else (out, airlight)
         if n > MAX_FRAMES_PER_CALL and not keep_maps:  # the library takes <= 65535 frames per call
@@ -112,7 +161,8 @@ class FrameEngine:
             for ev in events:
                 ev.record(st)
             ev_arr = (ctypes.c_void_p * len(events))(*[ev.cuda_event for ev in events])
-        with self._lock:
+        with self._lock, torch.cuda.device(dev):
+            self._order_after_last(st)
             if resize:
                 nbytes = self.lib.dhz_frames_resize_u8_workspace(n, h, w, H, W, ctypes.byref(p))
                 if nbytes == 0:
@@ -131,21 +181,8 @@ class FrameEngine:
                     frames.data_ptr(), 3 * H * W, n, H, W, ctypes.byref(p), out.data_ptr(), 3 * H * W,
                     airlight.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream, ev_arr)
                 _native.check(rc, "dhz_frames_u8")
-            maps = None
-            if keep_maps:
-                k = p.top_k
-                if resize:
-                    off = (ctypes.c_int64 * 5)()
-                    _native.check(self.lib.dhz_frames_resize_u8_layout(n, h, w, H, W, ctypes.byref(p), off),
-                                  "dhz_frames_resize_u8_layout")
-                    dark = ws[off[0]: off[0] + off[1] * n].view(torch.float64).view(n, H, W).clone()
-                    maps = {"dark_f64": dark}
-                else:
-                    off = self.layout(n, H, W, p)
-                    dark_fs = off[1]
-                    dark = ws[off[0]: off[0] + dark_fs * n].view(n, dark_fs)[:, : H * W].reshape(n, H, W).clone()
-                    maps = {"dark_u8": dark}
-                maps["selected"] = ws[off[2]: off[2] + 4 * n * k].view(torch.int32).view(n, k).clone()
+            maps = self._maps(ws, n, h, w, H, W, p, resize, st) if keep_maps else None
+            self._mark_done(st)
         if keep_maps:
             return out, airlight, maps
         return out, airlight
@@ -166,9 +203,10 @@ class StreamedEngine:
         self.streams = [torch.cuda.Stream(self.device) for _ in range(streams)]
 
     def run(self, frames, params, out=None, airlight=None, chunk=16):
-        n = frames.shape[0]
+        n, h, w = (int(v) for v in frames.shape[:3])
         if out is None:
-            out = torch.empty_like(frames)
+            H, W = FrameEngine.working_size(params, h, w)
+            out = torch.empty((n, H, W, 3), dtype=torch.uint8, device=frames.device)
         if airlight is None:
             airlight = torch.empty((n, 3), dtype=torch.float64, device=frames.device)
         cur = torch.cuda.current_stream(self.device)
@@ -200,8 +238,9 @@ class GraphedPipeline:
     def __init__(self, frames, params, out=None, airlight=None, streams=2, chunk=8, events=None):
         self.frames = frames
         self.params = params
-        self.out = out if out is not None else torch.empty_like(frames)
-        n = frames.shape[0]
+        n, h, w = (int(v) for v in frames.shape[:3])
+        H, W = FrameEngine.working_size(params, h, w)
+        self.out = out if out is not None else torch.empty((n, H, W, 3), dtype=torch.uint8, device=frames.device)
         self.airlight = airlight if airlight is not None else torch.empty(
             (n, 3), dtype=torch.float64, device=frames.device)
         self.streams = streams
