@@ -60,6 +60,21 @@ cudaError_t guided_recover_u8(const uint8_t* in, int64_t in_fs, int n, int H, in
                               const double* airlight, double omega, double t_min, const double* thr, double gamma,
                               bool balance, uint8_t* out, int64_t out_fs, void* ws, cudaStream_t st);
 
+// Image mode, one-pass guided filter with exact integer box sums (guided_fused.cu),
+// radius <= kFusedMaxRadius; the strip kernels above cover larger radii.
+constexpr int kFusedMaxRadius = 63;
+bool guided_fused_ok(int H, int W, int r);
+bool guided_use_fused(int H, int W, int r);
+size_t guided_fused_ws_bytes(int n, int H, int W, int r, bool balance);
+cudaError_t guided_fused_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, int r, double eps,
+                            const double* airlight, double omega, double t_min, const double* thr, double gamma,
+                            bool balance, uint8_t* out, int64_t out_fs, void* ws, cudaStream_t st);
+// Gray-world apply: bytes from t~ (fp64 [n][npx]), airlight and per-frame channel
+// thresholds / gains (balance_thresholds below).
+cudaError_t guided_apply(const uint8_t* in, int64_t in_fs, int n, int64_t npx, const double* t,
+                         const double* airlight, const double* thr, const float* gains, double gamma, uint8_t* out,
+                         int64_t out_fs, cudaStream_t st);
+
 // Gray-world balance from per-CTA channel sums of the gamma values (part[n][nparts][3]):
 // per frame and channel the gains and the 256 exact byte thresholds on the recovered
 // value (thr[n][3][256], thr[.][.][0] = -1, +inf for unreachable levels); gains[n][3]

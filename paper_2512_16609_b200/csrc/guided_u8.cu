@@ -12,7 +12,7 @@
 //
 // Box sums (replicate border == clamped indices, divisor (2r+1)^2 like the
 // reference's SAT) run as column-strip sliding sums: a CTA of 256 threads owns
-// 256*CPT input columns (CPT = 1 or 2 consecutive columns per thread; 256*CPT-2r
+// 256*CPT input columns (CPT = 1, 2 or 4 consecutive columns per thread, from the frame width; 256*CPT-2r
 // output columns) and a segment of rows; each thread keeps the vertical window
 // sums of its columns in fp64 registers (add the entering row, drop the leaving
 // one), and every output row takes its horizontal windows from a shared-memory
@@ -23,6 +23,8 @@
 // derives per-frame gains and exact per-channel byte thresholds (k_gf_thresholds)
 // and k_gf_apply only recovers and thresholds (no pow per pixel).
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "dhz_common.cuh"
 #include "dhz_internal.h"
@@ -499,6 +501,30 @@ int guided_seg_rows(int H, int W, int r, int cpt) {
   return std::min(seg, 1024);
 }
 
+cudaError_t guided_apply(const uint8_t* in, int64_t in_fs, int n, int64_t npx, const double* t,
+                         const double* airlight, const double* thr, const float* gains, double gamma, uint8_t* out,
+                         int64_t out_fs, cudaStream_t st) {
+  dim3 g2((unsigned)std::max<int64_t>(1, std::min<int64_t>(2048, (npx + 1023) / 1024)), n);
+  k_gf_apply<<<g2, 256, 0, st>>>(in, in_fs, npx, t, airlight, thr, gains, 1.0 / gamma, out, out_fs);
+  return cudaGetLastError();
+}
+
+// DHZ_GUIDED_PATH=fused|strip forces one image-mode implementation (tests, probes).
+static int guided_path_override() {
+  const char* s = getenv("DHZ_GUIDED_PATH");
+  if (!s) return 0;
+  if (!strcmp(s, "fused")) return 1;
+  if (!strcmp(s, "strip")) return 2;
+  return 0;
+}
+
+// The strip kernels stay the default: the one-pass exact kernel reads/writes ~10 B/px
+// instead of ~90 but is issue-bound and measured slower.
+bool guided_use_fused(int H, int W, int r) {
+  if (!guided_fused_ok(H, W, r)) return false;
+  return guided_path_override() == 1;
+}
+
 // Frames per chunk so the fp64 a/b (+t~) scratch stays within ~4 GB.
 int guided_chunk(int n, int H, int W, bool balance) {
   const double per = (balance ? 24.0 : 16.0) * (double)H * W;
@@ -506,6 +532,7 @@ int guided_chunk(int n, int H, int W, bool balance) {
 }
 
 size_t guided_ws_bytes(int n, int H, int W, int r, bool balance) {
+  if (guided_use_fused(H, W, r)) return guided_fused_ws_bytes(n, H, W, r, balance);
   const int64_t npx = (int64_t)H * W;
   const int c = guided_chunk(n, H, W, balance);
   size_t b = 16ull * npx * c;                                            // a, b
@@ -522,6 +549,9 @@ cudaError_t guided_recover_u8(const uint8_t* in, int64_t in_fs, int n, int H, in
                               const double* airlight, double omega, double t_min, const double* thr, double gamma,
                               bool balance, uint8_t* out, int64_t out_fs, void* ws, cudaStream_t st) {
   if (r < 1 || r > kGuidedMaxRadius) return cudaErrorInvalidValue;
+  if (guided_use_fused(H, W, r))
+    return guided_fused_u8(in, in_fs, n, H, W, r, eps, airlight, omega, t_min, thr, gamma, balance, out, out_fs, ws,
+                           st);
   const int64_t npx = (int64_t)H * W;
   const int chunk = guided_chunk(n, H, W, balance);
   const double inv_g = 1.0 / gamma;
@@ -539,9 +569,11 @@ cudaError_t guided_recover_u8(const uint8_t* in, int64_t in_fs, int n, int H, in
     double* b = a + npx * c;
     double* t = b + npx * c;
     double* part = t + npx * c;
+    cudaError_t ae = cudaSuccess;
     auto launch = [&](auto k1, auto k2, size_t sm1, size_t sm2) {
-      cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-      cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      if ((ae = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1)) != cudaSuccess ||
+          (ae = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
+        return;
       k1<<<grid, kThreads, sm1, st>>>(fin, in_fs, H, W, r, seg, eps, fA, omega, t_min, a, b);
       k2<<<grid, kThreads, sm2, st>>>(fin, in_fs, H, W, r, seg, a, b, fA, t_min, thr, inv_g, g1, fout, out_fs,
                                       balance ? t : nullptr, balance ? part : nullptr);
@@ -550,10 +582,12 @@ cudaError_t guided_recover_u8(const uint8_t* in, int64_t in_fs, int n, int H, in
       if (cpt == 4) launch(k_gf_pass1<4>, k_gf_pass2<0, 4>, pass_smem<4>(4), pass_smem<4>(2));
       else if (cpt == 2) launch(k_gf_pass1<2>, k_gf_pass2<0, 2>, pass_smem<2>(4), pass_smem<2>(2));
       else launch(k_gf_pass1<1>, k_gf_pass2<0, 1>, pass_smem<1>(4), pass_smem<1>(2));
+      if (ae != cudaSuccess) return ae;
     } else {
       if (cpt == 4) launch(k_gf_pass1<4>, k_gf_pass2<1, 4>, pass_smem<4>(4), pass_smem<4>(2));
       else if (cpt == 2) launch(k_gf_pass1<2>, k_gf_pass2<1, 2>, pass_smem<2>(4), pass_smem<2>(2));
       else launch(k_gf_pass1<1>, k_gf_pass2<1, 1>, pass_smem<1>(4), pass_smem<1>(2));
+      if (ae != cudaSuccess) return ae;
       const int nparts = grid.x * grid.y;
       double* bthr = part + 3LL * nparts * c;
       float* gains = reinterpret_cast<float*>(bthr + 3LL * 256 * c);
