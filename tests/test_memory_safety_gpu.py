@@ -1,0 +1,120 @@
+"""Memory-safety checks of the native pipelines without compute-sanitizer (which is
+closed on the B200 pool this package is tested on):
+
+* guard bands: input, output, airlight and workspace buffers sit inside larger
+  allocations whose margins hold a canary pattern; after the call every canary byte
+  must be intact (no out-of-bounds write) -- the input is read-only too;
+* poisoned memory: the same call with the workspace, the input margins and the
+  output prefilled with different patterns (0x00 / 0xFF / random) must give
+  bit-identical results (no read of uninitialised workspace, no read outside the
+  input frames that reaches an output);
+* determinism: repeated runs of the same batch are bit-identical (a data race on
+  shared memory or on the select/balance counters would show up as flips).
+Each native path is covered: video (vectorised and odd widths, balance), image
+mode (strip kernels and the fused kernel, balance on/off) and the default resize.
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+G = 4096  # guard bytes on each side
+
+
+def _cases():
+    from paper_2512_16609_b200 import DehazeParams
+
+    return [
+        ("video", DehazeParams(resize_to=None), (3, 136, 480)),
+        ("video-odd", DehazeParams(resize_to=None, patch_radius=4), (2, 37, 101)),
+        ("video-balance", DehazeParams(resize_to=None, white_balance=True), (2, 96, 384)),
+        ("image", DehazeParams.for_image(guided_radius=12), (2, 72, 256)),
+        ("image-odd", DehazeParams.for_image(guided_radius=5, white_balance=False), (2, 33, 77)),
+        ("image-wide", DehazeParams.for_image(patch_radius=15, guided_radius=60), (1, 70, 4100)),
+        ("resize", DehazeParams(resize_to=(160, 96)), (2, 192, 320)),
+        ("resize-balance", DehazeParams(resize_to=(97, 61), white_balance=True), (2, 120, 203)),
+    ]
+
+
+def _guarded(nbytes, fill, dev):
+    buf = torch.empty(G + nbytes + G, dtype=torch.uint8, device=dev)
+    buf.fill_(fill)
+    return buf
+
+
+def _run(frames, params, ws_fill, io_fill):
+    from paper_2512_16609_b200 import _native
+    from paper_2512_16609_b200.engine import FrameEngine, native_params
+    from paper_2512_16609_b200.quant import device_thresholds
+
+    lib = _native.lib()
+    dev = frames.device
+    n, h, w, _ = frames.shape
+    H, W = FrameEngine.working_size(params, h, w)
+    thr = device_thresholds(params.gamma, dev)
+    p = native_params(params, H * W, thr)
+    resize = (H, W) != (h, w)
+    fin = _guarded(3 * n * h * w, io_fill, dev)
+    fin[G:G + 3 * n * h * w].copy_(frames.reshape(-1))
+    fout = _guarded(3 * n * H * W, io_fill, dev)
+    fair = _guarded(24 * n, io_fill, dev)
+    if resize:
+        ws_bytes = lib.dhz_frames_resize_u8_workspace(n, h, w, H, W, ctypes.byref(p))
+    else:
+        ws_bytes = lib.dhz_frames_u8_workspace(n, H, W, ctypes.byref(p))
+    assert ws_bytes > 0
+    if isinstance(ws_fill, int):
+        ws = _guarded(ws_bytes, ws_fill, dev)
+    else:
+        ws = _guarded(ws_bytes, 0x33, dev)
+        ws[G:G + ws_bytes].copy_(torch.randint(0, 256, (ws_bytes,), dtype=torch.uint8, device=dev))
+    canaries = [(b, b[:G].clone(), b[-G:].clone()) for b in (fin, fout, fair, ws)]
+    frozen_in = fin.clone()
+    st = torch.cuda.current_stream(dev).cuda_stream
+    if resize:
+        rc = lib.dhz_frames_resize_u8(fin.data_ptr() + G, 3 * h * w, n, h, w, H, W, ctypes.byref(p),
+                                      fout.data_ptr() + G, 3 * H * W, fair.data_ptr() + G, ws.data_ptr() + G,
+                                      ws_bytes, st, None)
+    else:
+        rc = lib.dhz_frames_u8(fin.data_ptr() + G, 3 * H * W, n, H, W, ctypes.byref(p), fout.data_ptr() + G,
+                               3 * H * W, fair.data_ptr() + G, ws.data_ptr() + G, ws_bytes, st, None)
+    _native.check(rc, "dhz_frames")
+    torch.cuda.synchronize()
+    for b, lo, hi in canaries:
+        assert torch.equal(b[:G], lo) and torch.equal(b[-G:], hi), "guard band overwritten"
+    assert torch.equal(fin, frozen_in), "input modified"
+    return fout[G:-G].clone(), fair[G:-G].clone()
+
+
+@pytest.mark.parametrize("path", ["strip", "fused"])
+@pytest.mark.parametrize("case", range(8))
+def test_guards_and_poison(monkeypatch, path, case):
+    from paper_2512_16609_b200.synthetic import make_frames
+
+    name, params, (n, h, w) = _cases()[case]
+    if path == "fused" and params.mode != "image":
+        pytest.skip("fused kernel: image mode only")
+    monkeypatch.setenv("DHZ_GUIDED_PATH", path)
+    frames = make_frames("c3", frames=n, width=w, height=h, device="cuda")
+    ref_out, ref_air = _run(frames, params, 0x00, 0x00)
+    for ws_fill, io_fill in [(0xFF, 0xFF), ("random", 0x7F), (0x80, 0x01)]:
+        out, air = _run(frames, params, ws_fill, io_fill)
+        assert torch.equal(out, ref_out), f"{name}: output depends on memory contents"
+        assert torch.equal(air, ref_air), f"{name}: airlight depends on memory contents"
+
+
+@pytest.mark.parametrize("case", range(8))
+def test_repeat_determinism(case):
+    from paper_2512_16609_b200 import dehaze_batch
+    from paper_2512_16609_b200.synthetic import make_frames
+
+    name, params, (n, h, w) = _cases()[case]
+    frames = make_frames("c4", frames=n, width=w, height=h, device="cuda")
+    out0, air0 = dehaze_batch(frames, params)
+    for _ in range(12):
+        out, air = dehaze_batch(frames, params)
+        assert torch.equal(out, out0) and torch.equal(air, air0), name
