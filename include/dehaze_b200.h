@@ -84,6 +84,19 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int height, int width
  * postprocess + output.  Used for FrameTelemetry stage times. */
 #define DHZ_N_EVENTS 5
 
+/* The same pipeline in two halves, for the opt-in temporal stabilisation (the
+ * airlight trace is smoothed between them; paper_2512_16609_b200 pipeline
+ * `stabilise=`, not reference behaviour) and for multi-GPU runs that exchange the
+ * trace first.  _airlight runs K1-K4 (channel_min, min_filter, estimate_airlight:
+ * reference pipeline.py:182-190, estimation.py:46-84) and writes airlight (n x 3);
+ * _recover runs the remaining stages (pipeline.py:192-216) from a CALLER-GIVEN
+ * airlight.  dhz_frames_u8 == _airlight followed by _recover on the same workspace. */
+int dhz_frames_u8_airlight(const uint8_t* in, int64_t in_fs, int n, int height, int width, const dhz_params* p,
+                           double* airlight, void* ws, size_t ws_bytes, void* stream);
+int dhz_frames_u8_recover(const uint8_t* in, int64_t in_fs, int n, int height, int width, const dhz_params* p,
+                          const double* airlight, uint8_t* out, int64_t out_fs, void* ws, size_t ws_bytes,
+                          void* stream);
+
 /* Byte offsets inside the workspace after dhz_frames_u8 returned (valid until the
  * workspace is reused): [0] dark map u8 (n x H*W, frame stride [1]),
  * [2] selected airlight pixel indices uint32 (n x K, in summation order),
@@ -105,11 +118,41 @@ size_t dhz_frames_resize_u8_workspace(int n, int h, int w, int height, int width
 int dhz_frames_resize_u8(const uint8_t* in, int64_t in_fs, int n, int h, int w, int height, int width,
                          const dhz_params* p, uint8_t* out, int64_t out_fs, double* airlight, void* ws,
                          size_t ws_bytes, void* stream, void* const* events);
+/* Two halves of dhz_frames_resize_u8, as for the native size above. */
+int dhz_frames_resize_u8_airlight(const uint8_t* in, int64_t in_fs, int n, int h, int w, int height, int width,
+                                  const dhz_params* p, double* airlight, void* ws, size_t ws_bytes, void* stream);
+int dhz_frames_resize_u8_recover(const uint8_t* in, int64_t in_fs, int n, int h, int w, int height, int width,
+                                 const dhz_params* p, const double* airlight, uint8_t* out, int64_t out_fs,
+                                 void* ws, size_t ws_bytes, void* stream);
 /* Offsets after dhz_frames_resize_u8: [0] dark map float64 (n x height*width,
  * frame stride [1] bytes), [2] selected indices uint32 (n x K, summation order),
  * [3] -1, [4] total workspace bytes. */
 int dhz_frames_resize_u8_layout(int n, int h, int w, int height, int width, const dhz_params* p,
                                 int64_t* offsets5);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU (one process) and the opt-in airlight stabilisation.
+ * Video batches shard by frame into contiguous blocks, one per device (frames are
+ * independent: reference pipeline.py:257-260); the only exchange is the per-frame
+ * airlight trace (reference StreamStats.airlight_trace, pipeline.py:279,308).
+ * ------------------------------------------------------------------------- */
+/* Device group for dhz_allgather_airlight: enables peer access (NVLink) between the
+ * distinct devices; *comm receives an opaque handle.  A device may repeat (several
+ * shards on one GPU). */
+int dhz_comm_init(int ndev, const int* devices, void** comm);
+int dhz_comm_destroy(void* comm);
+/* All-gather of the per-device airlight blocks: device d holds counts[d] frames at
+ * send[d] (counts[d] x 3 doubles, on device d); afterwards recv[d] (sum(counts) x 3
+ * doubles on device d) holds every block in device order.  Enqueued on streams[d]
+ * (cudaStream_t on device d), ordered after the work already on every source
+ * stream; no host synchronisation. */
+int dhz_allgather_airlight(void* comm, const double* const* send, const int* counts, double* const* recv,
+                           void* const* streams);
+/* Opt-in temporal stabilisation (north_star; NOT reference behaviour):
+ * out[f] = lam * out[f-1] + (1 - lam) * trace[f] per channel, each product and sum
+ * rounded once, out[-1] = carry (3 doubles) or out[0] = trace[0] when carry is NULL.
+ * trace, out: n x 3 doubles (device, may alias only if equal); lam in [0, 1). */
+int dhz_ema_airlight(const double* trace, int n, double lam, const double* carry, double* out, void* stream);
 
 /* ---------------------------------------------------------------------------
  * float64 stage operations (reference public functions on float64 arrays; one

@@ -347,3 +347,57 @@ def quantize_after_gamma(x, gamma):
     x = np.asarray(x, dtype=np.float64)
     y = x.copy() if gamma == 1.0 else np.clip(np.power(x, 1.0 / gamma), 0.0, 1.0)
     return float_to_u8(y)
+
+
+# --------------------------------------------------------------------------
+# opt-in temporal stabilisation (north_star; NOT in the reference: SPEC.md:267
+# lists temporal smoothing as a non-goal).  Restated here only to check the
+# device recurrence bit for bit: plain Python floats are IEEE doubles with one
+# rounding per operation and no fused multiply-add.
+# --------------------------------------------------------------------------
+def ema_trace(trace, lam, carry=None):
+    """A'_f = lam * A'_{f-1} + (1 - lam) * A_f per channel; A'_-1 = carry, else A'_0 = A_0."""
+    keep, take = float(lam), 1.0 - float(lam)
+    out = []
+    prev = None if carry is None else [float(v) for v in carry]
+    for row in np.asarray(trace, dtype=np.float64):
+        cur = [float(v) for v in row]
+        if prev is not None:
+            cur = [keep * p + take * c for p, c in zip(prev, cur)]
+        out.append(cur)
+        prev = cur
+    return np.array(out, dtype=np.float64).reshape(-1, 3)
+
+
+def dehaze_stabilised(frames, params, lam):
+    """The stabilised clip: per-frame airlight -> ema_trace -> each frame recovered with A'."""
+    p = OracleParams.of(params)
+    airs = []
+    for f in frames:
+        m = {}
+        dehaze_frame(f, p, m)
+        airs.append(m["airlight"])
+    smooth = ema_trace(np.array(airs), lam)
+    outs = [dehaze_frame_with_airlight(f, p, a) for f, a in zip(frames, smooth)]
+    return outs, smooth
+
+
+def dehaze_frame_with_airlight(frame, params, airlight):
+    """pipeline.py:163-216 with the airlight given instead of estimated."""
+    p = OracleParams.of(params)
+    img = u8_to_float(frame)
+    if p.resize_to is not None:
+        w, h = p.resize_to
+        if (w, h) != (img.shape[1], img.shape[0]):
+            img = resize_bilinear(img, w, h)
+    cmin = channel_min(img)
+    a = np.asarray(airlight, dtype=np.float64)
+    t = transmission_from_channel_min(cmin, a, p.omega, p.t_min)
+    if p.mode == "image":
+        t = guided_filter(t, to_grayscale(img), p.guided_radius, p.guided_eps)
+        t = np.maximum(t, p.t_min)
+    out = recover_radiance(img, a, t)
+    out = gamma_correct(out, p.gamma)
+    if p.balance_enabled():
+        out = gray_world_balance(out)
+    return float_to_u8(out)

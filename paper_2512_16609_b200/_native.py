@@ -65,6 +65,20 @@ SIGNATURES = {
                                       _c_i64, _c_void_p, _c_void_p, _c_size, _c_void_p, _c_void_p]),
     "dhz_frames_resize_u8_layout": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _P,
                                              ctypes.POINTER(_c_i64)]),
+    "dhz_frames_u8_airlight": (_c_int, [_c_void_p, _c_i64, _c_int, _c_int, _c_int, _P, _c_void_p, _c_void_p,
+                                        _c_size, _c_void_p]),
+    "dhz_frames_u8_recover": (_c_int, [_c_void_p, _c_i64, _c_int, _c_int, _c_int, _P, _c_void_p, _c_void_p,
+                                       _c_i64, _c_void_p, _c_size, _c_void_p]),
+    "dhz_frames_resize_u8_airlight": (_c_int, [_c_void_p, _c_i64, _c_int, _c_int, _c_int, _c_int, _c_int, _P,
+                                               _c_void_p, _c_void_p, _c_size, _c_void_p]),
+    "dhz_frames_resize_u8_recover": (_c_int, [_c_void_p, _c_i64, _c_int, _c_int, _c_int, _c_int, _c_int, _P,
+                                              _c_void_p, _c_void_p, _c_i64, _c_void_p, _c_size, _c_void_p]),
+    # multi-GPU plumbing and the opt-in stabilisation
+    "dhz_comm_init": (_c_int, [_c_int, ctypes.POINTER(_c_int), ctypes.POINTER(_c_void_p)]),
+    "dhz_comm_destroy": (_c_int, [_c_void_p]),
+    "dhz_allgather_airlight": (_c_int, [_c_void_p, ctypes.POINTER(_c_void_p), ctypes.POINTER(_c_int),
+                                        ctypes.POINTER(_c_void_p), ctypes.POINTER(_c_void_p)]),
+    "dhz_ema_airlight": (_c_int, [_c_void_p, _c_int, ctypes.c_double, _c_void_p, _c_void_p, _c_void_p]),
     # float64 stage operations
     "dhz_f64_stats": (_c_int, [_c_void_p, _c_i64, _c_void_p, _c_void_p, _c_void_p]),
     "dhz_u8_to_f64": (_c_int, [_c_void_p, _c_i64, _c_void_p, _c_void_p]),

@@ -141,16 +141,16 @@ int dhz_frames_u8_layout(int n, int height, int width, const dhz_params* p, int6
   return DHZ_OK;
 }
 
-int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const dhz_params* p, uint8_t* out,
-                  int64_t out_fs, double* airlight, void* ws, size_t ws_bytes, void* stream,
-                  void* const* events) {
-  int rc = check_params(n, H, W, p);
-  if (rc) return rc;
-  if (n == 0) return DHZ_OK;
+}  // extern "C"
+
+namespace {
+
+// Shared argument checks of the native-size entry points.
+int frames_check(const uint8_t* in, int64_t in_fs, int n, int H, int W, const dhz_params* p, const void* out,
+                 int64_t out_fs, const double* airlight, void* ws, size_t ws_bytes, const Layout& L) {
   if (!in || !out || !airlight) return fail(DHZ_E_INVALID, "NULL array argument");
   const int64_t npx = (int64_t)H * W;
   if (in_fs < 3 * npx || out_fs < 3 * npx) return fail(DHZ_E_INVALID, "frame stride smaller than a frame");
-  const Layout L = make_layout(n, H, W, p);
   if (!ws || (int64_t)ws_bytes < L.total)
     return fail(DHZ_E_WORKSPACE, "workspace too small: need %lld bytes, got %zu", (long long)L.total, ws_bytes);
   if (p->mode == 1 && (p->guided_radius < 1 || p->guided_radius > dhz::kGuidedMaxRadius))
@@ -158,21 +158,23 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const d
                 p->guided_radius, dhz::kGuidedMaxRadius);
   if (dhz::dark_u8_max_smem(p->patch_radius) > 200 * 1024)
     return fail(DHZ_E_UNSUPPORTED, "patch_radius %d too large for the tiled erosion", p->patch_radius);
+  return DHZ_OK;
+}
 
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+// K1 dark channel + K2-K4 top-K select and airlight (events [0]..[2]).
+int frames_airlight(const uint8_t* in, int64_t in_fs, int n, int H, int W, const dhz_params* p, double* airlight,
+                    uint8_t* base, const Layout& L, cudaStream_t st, void* const* events) {
   auto mark = [&](int i) { record_stage_event(events, i, st); };
   mark(0);
-  uint8_t* base = static_cast<uint8_t*>(ws);
   cudaError_t e = cudaMemsetAsync(base, 0, (size_t)L.zero_end, st);  // maxima, select state, histograms
   if (e != cudaSuccess) return cuda_fail(e, "memset");
-
+  const int64_t npx = (int64_t)H * W;
   uint8_t* dark = base + L.dark;
   uint32_t* fmax = reinterpret_cast<uint32_t*>(base + L.frame_max);
   uint32_t* umax = reinterpret_cast<uint32_t*>(base + L.unit_max);
   e = dhz::dark_u8(in, in_fs, n, H, W, p->patch_radius, dark, L.dark_fs, fmax, umax, st);
   if (e != cudaSuccess) return cuda_fail(e, "dark_u8");
   mark(1);
-
   dhz::SelectWs sw{};
   sw.sel = reinterpret_cast<dhz::FrameSel*>(base + L.sel);
   sw.frame_max = fmax;
@@ -188,7 +190,16 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const d
   e = dhz::select_u8(dark, L.dark_fs, in, in_fs, n, npx, p->top_k, p->alpha, sw, airlight, st);
   if (e != cudaSuccess) return cuda_fail(e, "select_u8");
   mark(2);
+  return DHZ_OK;
+}
 
+// Transmission (+ guided filter) + recovery + postprocess + output from a given
+// airlight (events [3], [4]).
+int frames_recover(const uint8_t* in, int64_t in_fs, int n, int H, int W, const dhz_params* p,
+                   const double* airlight, uint8_t* out, int64_t out_fs, uint8_t* base, const Layout& L,
+                   cudaStream_t st, void* const* events) {
+  auto mark = [&](int i) { record_stage_event(events, i, st); };
+  cudaError_t e;
   if (p->mode == 1) {  // guided filter + recovery (+ gray-world) fused; event 3 == event 4
     e = dhz::guided_recover_u8(in, in_fs, n, H, W, p->guided_radius, p->guided_eps, airlight, p->omega, p->t_min,
                                p->thresholds, p->gamma, p->balance != 0, out, out_fs, base + L.tmap, st);
@@ -209,6 +220,47 @@ int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const d
   if (e != cudaSuccess) return cuda_fail(e, "recover_lut_u8");
   mark(4);
   return DHZ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dhz_frames_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, const dhz_params* p, uint8_t* out,
+                  int64_t out_fs, double* airlight, void* ws, size_t ws_bytes, void* stream,
+                  void* const* events) {
+  int rc = check_params(n, H, W, p);
+  if (rc) return rc;
+  if (n == 0) return DHZ_OK;
+  const Layout L = make_layout(n, H, W, p);
+  if ((rc = frames_check(in, in_fs, n, H, W, p, out, out_fs, airlight, ws, ws_bytes, L))) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  if ((rc = frames_airlight(in, in_fs, n, H, W, p, airlight, base, L, st, events))) return rc;
+  return frames_recover(in, in_fs, n, H, W, p, airlight, out, out_fs, base, L, st, events);
+}
+
+int dhz_frames_u8_airlight(const uint8_t* in, int64_t in_fs, int n, int H, int W, const dhz_params* p,
+                           double* airlight, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_params(n, H, W, p);
+  if (rc) return rc;
+  if (n == 0) return DHZ_OK;
+  const Layout L = make_layout(n, H, W, p);
+  if ((rc = frames_check(in, in_fs, n, H, W, p, airlight, 3LL * H * W, airlight, ws, ws_bytes, L))) return rc;
+  return frames_airlight(in, in_fs, n, H, W, p, airlight, static_cast<uint8_t*>(ws), L,
+                         reinterpret_cast<cudaStream_t>(stream), nullptr);
+}
+
+int dhz_frames_u8_recover(const uint8_t* in, int64_t in_fs, int n, int H, int W, const dhz_params* p,
+                          const double* airlight, uint8_t* out, int64_t out_fs, void* ws, size_t ws_bytes,
+                          void* stream) {
+  int rc = check_params(n, H, W, p);
+  if (rc) return rc;
+  if (n == 0) return DHZ_OK;
+  const Layout L = make_layout(n, H, W, p);
+  if ((rc = frames_check(in, in_fs, n, H, W, p, out, out_fs, airlight, ws, ws_bytes, L))) return rc;
+  return frames_recover(in, in_fs, n, H, W, p, airlight, out, out_fs, static_cast<uint8_t*>(ws), L,
+                        reinterpret_cast<cudaStream_t>(stream), nullptr);
 }
 
 /* ----------------------------------------------------------- resize path ---- */
@@ -281,21 +333,19 @@ int dhz_frames_resize_u8_layout(int n, int h, int w, int height, int width, cons
   return DHZ_OK;
 }
 
-int dhz_frames_resize_u8(const uint8_t* in, int64_t in_fs, int n, int h, int w, int H, int W, const dhz_params* p,
-                         uint8_t* out, int64_t out_fs, double* airlight, void* ws, size_t ws_bytes, void* stream,
-                         void* const* events) {
-  int rc = check_resize(n, h, w, H, W, p);
-  if (rc) return rc;
-  if (n == 0) return DHZ_OK;
+namespace {
+int resize_check(const uint8_t* in, int64_t in_fs, int n, int h, int w, int H, int W, const void* out,
+                 int64_t out_fs, const double* airlight, void* ws, size_t ws_bytes, const RLayout& L) {
   if (!in || !out || !airlight) return fail(DHZ_E_INVALID, "NULL array argument");
   if (in_fs < 3LL * h * w || out_fs < 3LL * H * W) return fail(DHZ_E_INVALID, "frame stride smaller than a frame");
-  const RLayout L = make_rlayout(n, H, W, p);
   if (!ws || (int64_t)ws_bytes < L.total)
     return fail(DHZ_E_WORKSPACE, "workspace too small: need %lld bytes, got %zu", (long long)L.total, ws_bytes);
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return DHZ_OK;
+}
+
+int resize_airlight(const uint8_t* in, int64_t in_fs, int n, const dhz::ResizeGeo& g, const dhz_params* p,
+                    double* airlight, uint8_t* base, const RLayout& L, cudaStream_t st, void* const* events) {
   auto mark = [&](int i) { record_stage_event(events, i, st); };
-  const dhz::ResizeGeo g = make_geo(h, w, H, W);
-  uint8_t* base = static_cast<uint8_t*>(ws);
   double* dark = reinterpret_cast<double*>(base + L.dark);
   uint32_t* hist = reinterpret_cast<uint32_t*>(base + L.hist);
   uint32_t* sel = reinterpret_cast<uint32_t*>(base + L.sel);
@@ -308,12 +358,57 @@ int dhz_frames_resize_u8(const uint8_t* in, int64_t in_fs, int n, int h, int w, 
   e = dhz::resize_select(in, in_fs, n, g, dark, hist, p->top_k, p->alpha, sel, airlight, st);
   if (e != cudaSuccess) return cuda_fail(e, "resize_select");
   mark(2);
-  mark(3);
-  e = dhz::resize_recover(in, in_fs, n, g, airlight, p->omega, p->t_min, p->thresholds, p->gamma, p->balance != 0,
-                          p->balance ? base + L.bal : nullptr, out, out_fs, st);
-  if (e != cudaSuccess) return cuda_fail(e, "resize_recover");
-  mark(4);
   return DHZ_OK;
+}
+
+int resize_recover_stage(const uint8_t* in, int64_t in_fs, int n, const dhz::ResizeGeo& g, const dhz_params* p,
+                         const double* airlight, uint8_t* out, int64_t out_fs, uint8_t* base, const RLayout& L,
+                         cudaStream_t st, void* const* events) {
+  record_stage_event(events, 3, st);
+  cudaError_t e = dhz::resize_recover(in, in_fs, n, g, airlight, p->omega, p->t_min, p->thresholds, p->gamma,
+                                      p->balance != 0, p->balance ? base + L.bal : nullptr, out, out_fs, st);
+  if (e != cudaSuccess) return cuda_fail(e, "resize_recover");
+  record_stage_event(events, 4, st);
+  return DHZ_OK;
+}
+}  // namespace
+
+int dhz_frames_resize_u8(const uint8_t* in, int64_t in_fs, int n, int h, int w, int H, int W, const dhz_params* p,
+                         uint8_t* out, int64_t out_fs, double* airlight, void* ws, size_t ws_bytes, void* stream,
+                         void* const* events) {
+  int rc = check_resize(n, h, w, H, W, p);
+  if (rc) return rc;
+  if (n == 0) return DHZ_OK;
+  const RLayout L = make_rlayout(n, H, W, p);
+  if ((rc = resize_check(in, in_fs, n, h, w, H, W, out, out_fs, airlight, ws, ws_bytes, L))) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const dhz::ResizeGeo g = make_geo(h, w, H, W);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  if ((rc = resize_airlight(in, in_fs, n, g, p, airlight, base, L, st, events))) return rc;
+  return resize_recover_stage(in, in_fs, n, g, p, airlight, out, out_fs, base, L, st, events);
+}
+
+int dhz_frames_resize_u8_airlight(const uint8_t* in, int64_t in_fs, int n, int h, int w, int H, int W,
+                                  const dhz_params* p, double* airlight, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_resize(n, h, w, H, W, p);
+  if (rc) return rc;
+  if (n == 0) return DHZ_OK;
+  const RLayout L = make_rlayout(n, H, W, p);
+  if ((rc = resize_check(in, in_fs, n, h, w, H, W, airlight, 3LL * H * W, airlight, ws, ws_bytes, L))) return rc;
+  return resize_airlight(in, in_fs, n, make_geo(h, w, H, W), p, airlight, static_cast<uint8_t*>(ws), L,
+                         reinterpret_cast<cudaStream_t>(stream), nullptr);
+}
+
+int dhz_frames_resize_u8_recover(const uint8_t* in, int64_t in_fs, int n, int h, int w, int H, int W,
+                                 const dhz_params* p, const double* airlight, uint8_t* out, int64_t out_fs, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  int rc = check_resize(n, h, w, H, W, p);
+  if (rc) return rc;
+  if (n == 0) return DHZ_OK;
+  const RLayout L = make_rlayout(n, H, W, p);
+  if ((rc = resize_check(in, in_fs, n, h, w, H, W, out, out_fs, airlight, ws, ws_bytes, L))) return rc;
+  return resize_recover_stage(in, in_fs, n, make_geo(h, w, H, W), p, airlight, out, out_fs,
+                              static_cast<uint8_t*>(ws), L, reinterpret_cast<cudaStream_t>(stream), nullptr);
 }
 
 }  // extern "C"

@@ -50,30 +50,60 @@ def gather_airlight_trace(local: torch.Tensor, n_frames: int, group=None) -> tor
     return torch.cat(parts, 0)
 
 
-def stabilise_trace(trace: torch.Tensor, lam: float) -> torch.Tensor:
-    """Opt-in EMA recurrence A'_f = lam * A'_{f-1} + (1 - lam) * A_f, A'_0 = A_0, as a scan.
+def stabilise_trace(trace: torch.Tensor, lam: float, carry: torch.Tensor | None = None) -> torch.Tensor:
+    """Opt-in EMA recurrence A'_f = lam * A'_{f-1} + (1 - lam) * A_f over an (n, 3) trace.
 
-    Closed form A'_f = lam^f A_0 + (1-lam) sum_{j=1..f} lam^(f-j) A_j, evaluated
-    with a cumulative sum of lam^-j-scaled terms in float64 (blocked to keep
-    lam^-j in range).  Not reference behaviour; never applied by default.
+    CUDA tensors run the library kernel (dhz_ema_airlight); CPU tensors the same
+    recurrence in float64 with the same roundings (one per product and sum), so
+    both give identical bits.  A'_-1 = ``carry`` when given, else A'_0 = A_0.  Not
+    reference behaviour; never applied by default.
     """
     if not 0.0 <= lam < 1.0:
         raise ValueError(f"lam must lie in [0, 1), got {lam}")
-    n = trace.shape[0]
-    if n == 0 or lam == 0.0:
-        return trace.clone()
-    out = torch.empty_like(trace)
-    block = 64
-    carry = trace[0].clone()
-    out[0] = carry
-    f = 1
-    while f < n:
-        m = min(block, n - f)
-        j = torch.arange(1, m + 1, dtype=trace.dtype, device=trace.device)
-        w = lam ** (-j)                                   # lam^-j, j = 1..m
-        terms = (1.0 - lam) * trace[f: f + m] * w[:, None]
-        pref = torch.cumsum(terms, 0) * (lam ** j)[:, None]
-        out[f: f + m] = pref + (lam ** j)[:, None] * carry
-        carry = out[f + m - 1].clone()
-        f += m
-    return out
+    if trace.is_cuda:
+        from .engine import ema_airlight
+
+        return ema_airlight(trace, lam, carry=carry)
+    a = trace.to(torch.float64).numpy()
+    out = a.copy()
+    keep, take = float(lam), 1.0 - float(lam)
+    prev = None if carry is None else [float(v) for v in carry]
+    for f in range(a.shape[0]):
+        cur = [float(v) for v in a[f]]
+        if prev is not None:
+            cur = [keep * p + take * c for p, c in zip(prev, cur)]
+        out[f] = cur
+        prev = cur
+    return torch.from_numpy(out)
+
+
+def dehaze_sharded(frames_local: torch.Tensor, params, n_frames: int, stabilise: float | None = None,
+                   group=None):
+    """One rank's part of a frame-sharded clip under torch.distributed (one process per GPU).
+
+    ``frames_local`` is this rank's contiguous block (shard_range) on its GPU.  The
+    rank runs the airlight half of the pipeline on its block, all-gathers the
+    per-frame airlight (NCCL over NVLink; 24 B/frame, the only exchange), optionally
+    smooths the global trace (``stabilise``, not reference behaviour) and recovers
+    its block with its slice of the trace.  Returns (out_local, airlight_trace) —
+    the trace is global, in frame order, identical on every rank.
+    """
+    from .engine import engine_for
+
+    if params is None:
+        from .pipeline import DehazeParams
+
+        params = DehazeParams()
+    params.validate()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    lo, hi = shard_range(n_frames, rank, world)
+    if frames_local.shape[0] != hi - lo:
+        raise ValueError(f"rank {rank} holds {frames_local.shape[0]} frames, shard_range gives {hi - lo}")
+    eng = engine_for(frames_local.device)
+    raw = eng.phase_airlight(frames_local, params)
+    trace = gather_airlight_trace(raw, n_frames, group=group)
+    if stabilise is not None:
+        trace = stabilise_trace(trace, float(stabilise))
+    out = eng.phase_recover(frames_local, params, trace[lo:hi].contiguous())
+    return out, trace

@@ -108,6 +108,71 @@ class FrameEngine:
         _native.check(self.lib.dhz_frames_u8_layout(n, H, W, ctypes.byref(p), off), "dhz_frames_u8_layout")
         return list(off)
 
+    def _ws_bytes(self, n, h, w, H, W, p):
+        if (H, W) != (h, w):
+            nbytes = self.lib.dhz_frames_resize_u8_workspace(n, h, w, H, W, ctypes.byref(p))
+        else:
+            nbytes = self.lib.dhz_frames_u8_workspace(n, H, W, ctypes.byref(p))
+        if nbytes == 0:
+            _native.check(_native.DHZ_E_INVALID, "workspace query")
+        return nbytes
+
+    def phase_airlight(self, frames, params, airlight=None, stream=None):
+        """First half of the pipeline (dark channel + top-K select): the (n, 3) airlight."""
+        n, h, w, _ = frames.shape
+        H, W = self.working_size(params, h, w)
+        dev = frames.device
+        if airlight is None:
+            airlight = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        else:
+            _check_buffer(airlight, "airlight", (n, 3), torch.float64, dev)
+        if n == 0:
+            return airlight
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        p = native_params(params, H * W, device_thresholds(params.gamma, dev))
+        with self._lock, torch.cuda.device(dev):
+            self._order_after_last(st)
+            ws = self.workspace(self._ws_bytes(n, h, w, H, W, p))
+            if (H, W) != (h, w):
+                rc = self.lib.dhz_frames_resize_u8_airlight(frames.data_ptr(), 3 * h * w, n, h, w, H, W,
+                                                            ctypes.byref(p), airlight.data_ptr(), ws.data_ptr(),
+                                                            ws.numel(), st.cuda_stream)
+            else:
+                rc = self.lib.dhz_frames_u8_airlight(frames.data_ptr(), 3 * H * W, n, H, W, ctypes.byref(p),
+                                                     airlight.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)
+            _native.check(rc, "dhz_frames_*_airlight")
+            self._mark_done(st)
+        return airlight
+
+    def phase_recover(self, frames, params, airlight, out=None, stream=None):
+        """Second half (transmission [+ guided filter], recovery, output) from a given airlight."""
+        n, h, w, _ = frames.shape
+        H, W = self.working_size(params, h, w)
+        dev = frames.device
+        _check_buffer(airlight, "airlight", (n, 3), torch.float64, dev)
+        if out is None:
+            out = torch.empty((n, H, W, 3), dtype=torch.uint8, device=dev)
+        else:
+            _check_buffer(out, "out", (n, H, W, 3), torch.uint8, dev)
+        if n == 0:
+            return out
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        p = native_params(params, H * W, device_thresholds(params.gamma, dev))
+        with self._lock, torch.cuda.device(dev):
+            self._order_after_last(st)
+            ws = self.workspace(self._ws_bytes(n, h, w, H, W, p))
+            if (H, W) != (h, w):
+                rc = self.lib.dhz_frames_resize_u8_recover(frames.data_ptr(), 3 * h * w, n, h, w, H, W,
+                                                           ctypes.byref(p), airlight.data_ptr(), out.data_ptr(),
+                                                           3 * H * W, ws.data_ptr(), ws.numel(), st.cuda_stream)
+            else:
+                rc = self.lib.dhz_frames_u8_recover(frames.data_ptr(), 3 * H * W, n, H, W, ctypes.byref(p),
+                                                    airlight.data_ptr(), out.data_ptr(), 3 * H * W, ws.data_ptr(),
+                                                    ws.numel(), st.cuda_stream)
+            _native.check(rc, "dhz_frames_*_recover")
+            self._mark_done(st)
+        return out
+
     @staticmethod
     def working_size(params, H, W):
         """(height, width) the pipeline runs at: resize_to, or the native size."""
@@ -118,7 +183,8 @@ class FrameEngine:
 
     def run(self, frames: torch.Tensor, params, out: torch.Tensor | None = None,
             airlight: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None,
-            keep_maps: bool = False, events=None):
+            keep_maps: bool = False, events=None, stabilise: float | None = None,
+            carry: torch.Tensor | None = None):
         """Dehaze ``frames`` (n, H, W, 3) uint8 CUDA, C-contiguous.
 
         Frames are first resized to ``params.resize_to`` when that differs from
@@ -126,6 +192,11 @@ class FrameEngine:
         (n, H', W', 3), airlight float64 (n, 3)) as CUDA tensors, plus a dict of
         device maps when ``keep_maps`` (dark map — u8 at native size, float64
         after a resize — and the selected indices).
+
+        ``stabilise=lam`` (opt-in, NOT reference behaviour): the frames' airlight
+        trace is smoothed by the recurrence A'_f = lam A'_{f-1} + (1 - lam) A_f
+        (dhz_ema_airlight; A'_-1 = ``carry`` (3,) when given) between the airlight
+        and the recovery halves of the pipeline; the returned airlight is A'.
         """
         if frames.dim() != 4 or frames.shape[-1] != 3 or frames.dtype != torch.uint8:
             raise ValueError(f"frames must be (n, H, W, 3) uint8, got {tuple(frames.shape)} {frames.dtype}")
@@ -151,9 +222,17 @@ class FrameEngine:
         if n > MAX_FRAMES_PER_CALL and not keep_maps:  # the library takes <= 65535 frames per call
             for lo in range(0, n, MAX_FRAMES_PER_CALL):
                 hi = min(n, lo + MAX_FRAMES_PER_CALL)
-                self.run(frames[lo:hi], params, out=out[lo:hi], airlight=airlight[lo:hi], stream=stream)
+                self.run(frames[lo:hi], params, out=out[lo:hi], airlight=airlight[lo:hi], stream=stream,
+                         stabilise=stabilise, carry=carry if lo == 0 else airlight[lo - 1])
             return out, airlight
         st = stream if stream is not None else torch.cuda.current_stream(dev)
+        if stabilise is not None:
+            if keep_maps or events is not None:
+                raise ValueError("stabilise= runs the two-phase path (no maps / stage events)")
+            raw = self.phase_airlight(frames, params, stream=st)
+            ema_airlight(raw, stabilise, carry=carry, out=airlight, stream=st)
+            self.phase_recover(frames, params, airlight, out=out, stream=st)
+            return out, airlight
         ev_arr = None
         if events is not None:
             # torch creates events lazily: record once so each has a handle, then
@@ -185,6 +264,124 @@ class FrameEngine:
             self._mark_done(st)
         if keep_maps:
             return out, airlight, maps
+        return out, airlight
+
+
+def ema_airlight(trace: torch.Tensor, lam: float, carry: torch.Tensor | None = None,
+                 out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Opt-in temporal stabilisation of an (n, 3) float64 CUDA airlight trace
+    (dhz_ema_airlight): A'_f = lam A'_{f-1} + (1 - lam) A_f, each product and sum
+    rounded once; A'_-1 = ``carry`` when given, else A'_0 = A_0.  NOT reference
+    behaviour (reference SPEC.md:267 lists temporal smoothing as a non-goal)."""
+    lam = float(lam)
+    if not 0.0 <= lam < 1.0:
+        raise ValueError(f"stabilise must lie in [0, 1), got {lam}")
+    n = int(trace.shape[0])
+    dev = trace.device
+    trace = trace.contiguous()
+    if out is None:
+        out = torch.empty_like(trace)
+    if carry is not None:
+        carry = carry.to(device=dev, dtype=torch.float64).contiguous()
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        rc = _native.lib().dhz_ema_airlight(trace.data_ptr(), n, lam, carry.data_ptr() if carry is not None else None,
+                                            out.data_ptr(), st.cuda_stream)
+    _native.check(rc, "dhz_ema_airlight")
+    return out
+
+
+class DeviceGroup:
+    """Several GPUs (or several shards on one GPU) behind dhz_comm_init: one engine and
+    one stream per shard, and the airlight all-gather between them."""
+
+    def __init__(self, devices):
+        devs = [torch.device("cuda", d) if isinstance(d, int) else torch.device(d) for d in devices]
+        if not devs:
+            raise ValueError("devices must name at least one CUDA device")
+        for d in devs:
+            if d.type != "cuda":
+                raise ValueError(f"devices must be CUDA devices, got {d}")
+        self.devices = [torch.device("cuda", d.index if d.index is not None else torch.cuda.current_device())
+                        for d in devs]
+        self.lib = _native.lib()
+        self.engines = [FrameEngine(d) for d in self.devices]
+        self.streams = [torch.cuda.Stream(d) for d in self.devices]
+        ids = (ctypes.c_int * len(self.devices))(*[d.index for d in self.devices])
+        h = ctypes.c_void_p()
+        _native.check(self.lib.dhz_comm_init(len(self.devices), ids, ctypes.byref(h)), "dhz_comm_init")
+        self._comm = h
+
+    def __del__(self):
+        if getattr(self, "_comm", None):
+            try:
+                self.lib.dhz_comm_destroy(self._comm)
+            except Exception:
+                pass
+            self._comm = None
+
+    def allgather_airlight(self, blocks, counts):
+        """blocks[d]: (counts[d], 3) float64 on device d -> per device the (sum, 3) trace."""
+        total = sum(counts)
+        k = len(self.devices)
+        recv = [torch.empty((total, 3), dtype=torch.float64, device=d) for d in self.devices]
+        send_p = (ctypes.c_void_p * k)(*[b.data_ptr() for b in blocks])
+        recv_p = (ctypes.c_void_p * k)(*[r.data_ptr() for r in recv])
+        cnt = (ctypes.c_int * k)(*counts)
+        sts = (ctypes.c_void_p * k)(*[s.cuda_stream for s in self.streams])
+        _native.check(self.lib.dhz_allgather_airlight(self._comm, send_p, cnt, recv_p, sts), "dhz_allgather_airlight")
+        return recv
+
+    def run(self, frames: torch.Tensor, params, out: torch.Tensor | None = None, stabilise: float | None = None):
+        """Dehaze a (n, H, W, 3) uint8 batch (host or any device) sharded by frame over the
+        group: contiguous blocks (shard_range), each dehazed on its device; the airlight
+        trace is all-gathered (every device holds it in frame order) and, with
+        ``stabilise``, smoothed on every device before the recovery half.  Returns
+        (out, airlight) on ``frames``' device (outputs copied back in frame order)."""
+        from .distributed import shard_range
+
+        n, h, w = (int(v) for v in frames.shape[:3])
+        H, W = FrameEngine.working_size(params, h, w)
+        home = frames.device if frames.is_cuda else self.devices[0]
+        if out is None:
+            out = torch.empty((n, H, W, 3), dtype=torch.uint8, device=home)
+        airlight = torch.empty((n, 3), dtype=torch.float64, device=home)
+        if n == 0:
+            return out, airlight
+        k = len(self.devices)
+        ranges = [shard_range(n, i, k) for i in range(k)]
+        cur = torch.cuda.current_stream(home) if frames.is_cuda else None
+        locals_ = []
+        for i, (lo, hi) in enumerate(ranges):
+            dev, st = self.devices[i], self.streams[i]
+            if cur is not None:
+                st.wait_stream(cur)
+            with torch.cuda.stream(st):
+                src = frames[lo:hi]
+                f_d = src if (src.is_cuda and src.device == dev) else src.to(dev, non_blocking=True)
+                raw = self.engines[i].phase_airlight(f_d, params, stream=st) if hi > lo else \
+                    torch.empty((0, 3), dtype=torch.float64, device=dev)
+            locals_.append((f_d, raw))
+        traces = self.allgather_airlight([r for _, r in locals_], [hi - lo for lo, hi in ranges])
+        for i, (lo, hi) in enumerate(ranges):
+            dev, st = self.devices[i], self.streams[i]
+            f_d, _ = locals_[i]
+            with torch.cuda.stream(st):
+                trace = traces[i]
+                if stabilise is not None:
+                    trace = ema_airlight(trace, stabilise, stream=st)
+                if i == 0:
+                    airlight.copy_(trace, non_blocking=True)
+                if hi > lo:
+                    mine = trace[lo:hi]
+                    o_d = self.engines[i].phase_recover(f_d, params, mine, stream=st)
+                    out[lo:hi].copy_(o_d, non_blocking=True)
+        if cur is not None:
+            for st in self.streams:
+                cur.wait_stream(st)
+        else:
+            for st in self.streams:
+                st.synchronize()
         return out, airlight
 
 

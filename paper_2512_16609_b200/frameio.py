@@ -143,7 +143,7 @@ def dehaze_raw_stream(src, dst, header, params=None):
         trace.append(air)
         count += 1
 
-    pipe = _StreamPipe(_device(), params, (H, W, 3), fresh=False)
+    pipe = _StreamPipe([_device()], params, (H, W, 3), fresh=False)
     size = header.frame_bytes
     produced = 0
     err = None

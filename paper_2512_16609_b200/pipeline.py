@@ -209,6 +209,48 @@ def _as_device_batch(frames_np, device):
     return t.to(device=device, non_blocking=False)
 
 
+def _check_stabilise(stabilise):
+    """stabilise=None (reference behaviour) or the EMA weight lam in [0, 1)."""
+    if stabilise is None:
+        return None
+    lam = float(stabilise)
+    if not 0.0 <= lam < 1.0:
+        raise ValueError(f"stabilise must be None or lie in [0, 1), got {stabilise!r}")
+    return lam
+
+
+def _device_list(devices):
+    """devices=None -> None; else a list of torch CUDA devices (repeats allowed)."""
+    if devices is None:
+        return None
+    import torch
+
+    out = []
+    for d in devices:
+        d = torch.device("cuda", d) if isinstance(d, int) else torch.device(d)
+        if d.type != "cuda":
+            raise ValueError(f"devices must be CUDA devices, got {d}")
+        out.append(torch.device("cuda", d.index if d.index is not None else torch.cuda.current_device()))
+    if not out:
+        raise ValueError("devices must name at least one CUDA device")
+    return out
+
+
+_groups: dict = {}
+
+
+def _group(devs):
+    from .engine import DeviceGroup
+
+    import threading
+
+    key = (tuple(d.index for d in devs), threading.get_ident())
+    g = _groups.get(key)
+    if g is None:
+        g = _groups[key] = DeviceGroup(devs)
+    return g
+
+
 def _run_native(batch, params, telemetry=None, keep_maps=False):
     """batch: (n, H, W, 3) uint8 CUDA tensor at its working size."""
     import torch
@@ -287,18 +329,33 @@ def dehaze_image(frame, params=None, telemetry=None):
     return dehaze_frame(frame, params, telemetry)
 
 
-def dehaze_batch(frames, params=None, out=None):
+def dehaze_batch(frames, params=None, out=None, devices=None, stabilise=None):
     """Dehaze a device-resident batch (n, H, W, 3) uint8 CUDA tensor in one pipeline launch.
 
     Returns (out, airlight) CUDA tensors: out (n, H', W', 3) uint8, airlight
     (n, 3) float64, with (H', W') the working size (resize_to in video mode).
     Calls the batched native path does not cover (see _native_ok) run the
     per-frame float64 device path.
+
+    ``devices`` (list of CUDA devices, repeats allowed): shard the batch by frame
+    over them (contiguous blocks; the airlight trace is all-gathered through
+    dhz_allgather_airlight); results are bit-identical to one device.
+    ``stabilise=lam`` (opt-in, NOT reference behaviour, reference SPEC.md:267):
+    smooth the airlight trace with A'_f = lam A'_{f-1} + (1 - lam) A_f before the
+    recovery; the returned airlight is A'.
     """
     if params is None:
         params = DehazeParams()
     params.validate()
+    lam = _check_stabilise(stabilise)
+    devs = _device_list(devices)
     n, h, w = int(frames.shape[0]), int(frames.shape[1]), int(frames.shape[2])
+    if (devs is not None or lam is not None) and not _native_ok(params, h, w):
+        raise ValueError("devices= / stabilise= need a call the batched native pipeline covers "
+                         "(see _native_ok: image mode with a resize, map capture, guided_radius > "
+                         f"{GUIDED_MAX_RADIUS} or patch_radius > {RESIZE_MAX_RADIUS} after a resize are not)")
+    if devs is not None:
+        return _group(devs).run(frames, params, out=out, stabilise=lam)
     if not _native_ok(params, h, w):
         import torch
 
@@ -316,7 +373,7 @@ def dehaze_batch(frames, params=None, out=None):
         return torch.stack(outs), torch.stack(airs)
     from .engine import engine_for
 
-    return engine_for(frames.device).run(frames, params, out=out)
+    return engine_for(frames.device).run(frames, params, out=out, stabilise=lam)
 
 
 class _HostPipe:
@@ -332,25 +389,44 @@ class _HostPipe:
         self.din = [torch.empty((chunk, H, W, 3), dtype=torch.uint8, device=dev) for _ in range(slots)]
         self.dout = [torch.empty((chunk, OH, OW, 3), dtype=torch.uint8, device=dev) for _ in range(slots)]
         self.dair = [torch.empty((chunk, 3), dtype=torch.float64, device=dev) for _ in range(slots)]
+        self.carry = torch.zeros(3, dtype=torch.float64, device=dev)  # stabilise: A' carried across chunks
 
 
 _host_pipes: dict = {}
 
 
-def dehaze_host_batch(frames, params=None, out=None, airlight=None, chunk=None):
+def dehaze_host_batch(frames, params=None, out=None, airlight=None, chunk=None, devices=None, stabilise=None):
     """Dehaze a HOST batch (n, H, W, 3) uint8 torch tensor (pinned for overlap) end to end.
 
     Frames move to the GPU in chunks on a ring of streams: H2D copy, fused
     pipeline and D2H copy of chunk c overlap those of chunks c-1 and c+1.
     Returns (out, airlight) host tensors (pinned when allocated here); out has
-    the working size (resize_to in video mode).
+    the working size (resize_to in video mode).  ``devices``: one ring per device
+    over its contiguous block of frames (all devices copy and compute at once);
+    ``stabilise``: as in dehaze_batch (the recurrence runs chunk by chunk in frame
+    order, carrying A' across chunks).
     """
     import torch
 
     if params is None:
         params = DehazeParams()
     params.validate()
+    lam = _check_stabilise(stabilise)
+    devs = _device_list(devices)
     n, H, W = int(frames.shape[0]), int(frames.shape[1]), int(frames.shape[2])
+    if (devs is not None or lam is not None) and not _native_ok(params, H, W):
+        raise ValueError("devices= / stabilise= need a call the batched native pipeline covers (see _native_ok)")
+    if devs is not None and lam is not None and len(devs) > 1:
+        # the recurrence needs every earlier frame's airlight: keep the shards resident
+        o, a = _group(devs).run(frames, params, stabilise=lam)
+        o, a = o.cpu(), a.cpu()
+        if out is not None:
+            out.copy_(o)
+            o = out
+        if airlight is not None:
+            airlight.copy_(a)
+            a = airlight
+        return o, a
     if not _native_ok(params, H, W):
         # resize / very wide guided windows: float64 device path, frame by frame
         o, a = dehaze_batch(frames.to(_device()), params)
@@ -361,9 +437,10 @@ def dehaze_host_batch(frames, params=None, out=None, airlight=None, chunk=None):
             airlight.copy_(a)
             a = airlight
         return o.cpu() if o.is_cuda else o, a.cpu() if a.is_cuda else a
-    dev = _device()
+    from .distributed import shard_range
     from .engine import FrameEngine
 
+    devs = devs if devs is not None else [_device()]
     OH, OW = FrameEngine.working_size(params, H, W)
     if out is None:
         out = torch.empty((n, OH, OW, 3), dtype=torch.uint8, pin_memory=True)
@@ -375,26 +452,47 @@ def dehaze_host_batch(frames, params=None, out=None, airlight=None, chunk=None):
         chunk = max(1, min(n, (48 << 20) // (3 * H * W)))
     import threading
 
-    # per thread, like engine_for: concurrent callers never share staging buffers
-    key = (dev.index, threading.get_ident(), chunk, H, W, OH, OW)
-    pipe = _host_pipes.get(key)
-    if pipe is None:
-        pipe = _host_pipes[key] = _HostPipe(dev, chunk, H, W, OH, OW)
-    cur = torch.cuda.current_stream(dev)
-    for st in pipe.streams:
-        st.wait_stream(cur)
-    for c, lo in enumerate(range(0, n, chunk)):
-        s = c % len(pipe.streams)
-        st = pipe.streams[s]
-        m = min(chunk, n - lo)
-        with torch.cuda.stream(st):
-            pipe.din[s][:m].copy_(frames[lo: lo + m], non_blocking=True)
-            pipe.engines[s].run(pipe.din[s][:m], params, out=pipe.dout[s][:m], airlight=pipe.dair[s][:m],
-                                stream=st)
-            out[lo: lo + m].copy_(pipe.dout[s][:m], non_blocking=True)
-            airlight[lo: lo + m].copy_(pipe.dair[s][:m], non_blocking=True)
-    for st in pipe.streams:
-        st.synchronize()
+    # per (device, thread), like engine_for: concurrent callers never share staging buffers;
+    # a device listed twice gets two rings
+    pipes, plans = [], []
+    for i, dev in enumerate(devs):
+        key = (dev.index, i, threading.get_ident(), chunk, H, W, OH, OW)
+        pipe = _host_pipes.get(key)
+        if pipe is None:
+            pipe = _host_pipes[key] = _HostPipe(dev, chunk, H, W, OH, OW)
+        cur = torch.cuda.current_stream(dev)
+        for st in pipe.streams:
+            st.wait_stream(cur)
+        lo, hi = shard_range(n, i, len(devs))
+        pipes.append(pipe)
+        plans.append(list(range(lo, hi, chunk)))
+    carry = None  # stabilise: A' of the last frame before the chunk (single device: in frame order)
+    carry_ev = None
+    for c in range(max(len(p) for p in plans)):
+        for i, pipe in enumerate(pipes):  # interleave: every device's ring advances each round
+            if c >= len(plans[i]):
+                continue
+            lo = plans[i][c]
+            hi = min(lo + chunk, shard_range(n, i, len(devs))[1])
+            s = c % len(pipe.streams)
+            st = pipe.streams[s]
+            m = hi - lo
+            with torch.cuda.stream(st):
+                pipe.din[s][:m].copy_(frames[lo: hi], non_blocking=True)
+                if lam is not None and carry_ev is not None:
+                    st.wait_event(carry_ev)
+                pipe.engines[s].run(pipe.din[s][:m], params, out=pipe.dout[s][:m], airlight=pipe.dair[s][:m],
+                                    stream=st, stabilise=lam, carry=carry)
+                if lam is not None:
+                    carry = pipe.carry
+                    carry.copy_(pipe.dair[s][m - 1], non_blocking=True)
+                    carry_ev = torch.cuda.Event()
+                    carry_ev.record(st)
+                out[lo: hi].copy_(pipe.dout[s][:m], non_blocking=True)
+                airlight[lo: hi].copy_(pipe.dair[s][:m], non_blocking=True)
+    for pipe in pipes:
+        for st in pipe.streams:
+            st.synchronize()
     return out, airlight
 
 
@@ -413,9 +511,13 @@ class _StreamPipe:
     stream) and the host goes on filling the next slot, so PCIe transfers and
     kernels of batch k overlap the host copies of batch k+1.  Slots are drained
     (outputs handed to the sink) in submission order, which keeps frame order.
+    With several devices the slots alternate between them (slot k on device
+    k mod ndev), so consecutive batches run on different GPUs at the same time.
+    With ``stabilise`` each batch's recurrence starts from the previous batch's
+    last A' (an event chain across the slots; the carry hops devices if needed).
     """
 
-    def __init__(self, dev, params, shape, fresh=True):
+    def __init__(self, devs, params, shape, fresh=True, stabilise=None):
         import torch
 
         from .engine import FrameEngine
@@ -424,21 +526,25 @@ class _StreamPipe:
         OH, OW = FrameEngine.working_size(params, H, W)
         self.batch = max(1, min(_STREAM_BATCH_MAX, _PIPE_BATCH_BYTES // (3 * H * W)))
         self.params = params
+        self.lam = stabilise
         self.out_shape = (OH, OW, 3)
-        S, B = _PIPE_SLOTS, self.batch
+        S, B = _PIPE_SLOTS * len(devs), self.batch
+        sdev = [devs[k % len(devs)] for k in range(S)]
         pin = dict(dtype=torch.uint8, pin_memory=True)
         self.hin = [torch.empty((B, H, W, 3), **pin) for _ in range(S)]
         self.hout = [torch.empty((B, OH, OW, 3), **pin) for _ in range(S)]
         self.hair = [torch.empty((B, 3), dtype=torch.float64, pin_memory=True) for _ in range(S)]
-        self.din = [torch.empty((B, H, W, 3), dtype=torch.uint8, device=dev) for _ in range(S)]
-        self.dout = [torch.empty((B, OH, OW, 3), dtype=torch.uint8, device=dev) for _ in range(S)]
-        self.dair = [torch.empty((B, 3), dtype=torch.float64, device=dev) for _ in range(S)]
-        self.streams = [torch.cuda.Stream(dev) for _ in range(S)]
-        self.engines = [FrameEngine(dev) for _ in range(S)]
+        self.din = [torch.empty((B, H, W, 3), dtype=torch.uint8, device=d) for d in sdev]
+        self.dout = [torch.empty((B, OH, OW, 3), dtype=torch.uint8, device=d) for d in sdev]
+        self.dair = [torch.empty((B, 3), dtype=torch.float64, device=d) for d in sdev]
+        self.carry = [torch.zeros(3, dtype=torch.float64, device=d) for d in sdev]
+        self.streams = [torch.cuda.Stream(d) for d in sdev]
+        self.engines = [FrameEngine(d) for d in sdev]
         self.events = [torch.cuda.Event() for _ in range(S)]
         self.inflight = [0] * S
         self.slot = 0
         self.fill = 0
+        self.prev = None  # (slot, rows) of the last submitted batch (stabilise carry source)
         self.fresh = fresh  # False: emit views of the pinned output (the consumer copies at once)
         self._emit = None
 
@@ -470,12 +576,19 @@ class _StreamPipe:
         st = self.streams[s]
         with torch.cuda.stream(st):
             self.din[s][:m].copy_(self.hin[s][:m], non_blocking=True)
+            carry = None
+            if self.lam is not None and self.prev is not None:
+                p, pm = self.prev
+                st.wait_event(self.events[p])
+                self.carry[s].copy_(self.dair[p][pm - 1], non_blocking=True)
+                carry = self.carry[s]
             self.engines[s].run(self.din[s][:m], self.params, out=self.dout[s][:m], airlight=self.dair[s][:m],
-                                stream=st)
+                                stream=st, stabilise=self.lam, carry=carry)
             self.hout[s][:m].copy_(self.dout[s][:m], non_blocking=True)
             self.hair[s][:m].copy_(self.dair[s][:m], non_blocking=True)
             self.events[s].record(st)
         self.inflight[s] = m
+        self.prev = (s, m)
         self.slot = (s + 1) % len(self.hin)
         self.fill = 0
 
@@ -502,7 +615,7 @@ class _StreamPipe:
             self.drain((self.slot + k) % S, emit)
 
 
-def process_stream(frames, params=None, sink=None, workers=1):
+def process_stream(frames, params=None, sink=None, workers=1, devices=None, stabilise=None):
     """Run the pipeline over an iterable of uint8 frames, in order (reference pipeline.py:232-308).
 
     Frames are validated as they arrive and dehazed in device batches; each
@@ -510,6 +623,11 @@ def process_stream(frames, params=None, sink=None, workers=1):
     raises after every frame before it has been dehazed and handed to the sink.
     On the native paths the batches are pipelined (``_StreamPipe``); ``workers``
     keeps the reference's contract (>= 1; results never depend on it).
+    Additions (defaults = reference behaviour): ``devices`` spreads consecutive
+    batches over several GPUs (the multi-GPU stand-in for the reference's thread
+    fan-out, pipeline.py:282-304); ``stabilise=lam`` smooths the airlight trace
+    (A'_f = lam A'_{f-1} + (1 - lam) A_f; not reference behaviour),
+    and the trace then records A'.
     """
     if params is None:
         params = DehazeParams()
@@ -517,6 +635,8 @@ def process_stream(frames, params=None, sink=None, workers=1):
     workers = int(workers)
     if workers < 1:
         raise ValueError(f"workers must be >= 1, got {workers}")
+    lam = _check_stabilise(stabilise)
+    devs = _device_list(devices)
 
     trace = []
     count = 0
@@ -568,7 +688,10 @@ def process_stream(frames, params=None, sink=None, workers=1):
                 per = frame.nbytes
                 limit = max(1, min(_STREAM_BATCH_MAX, _STREAM_BATCH_BYTES // max(per, 1)))
                 if _native_ok(params, frame.shape[0], frame.shape[1]):
-                    pipe = _StreamPipe(dev, params, frame.shape)
+                    pipe = _StreamPipe(devs if devs is not None else [dev], params, frame.shape, stabilise=lam)
+                elif devs is not None or lam is not None:
+                    raise ValueError("devices= / stabilise= need a call the batched native pipeline covers "
+                                     "(see _native_ok)")
             elif frame.shape != expected_shape:
                 raise ValueError(
                     f"frame {index} has size {frame.shape[1]}x{frame.shape[0]}, "

@@ -158,3 +158,56 @@ def test_airlight_trace_allgather_gloo(n):
     want = np.arange(n * 3, dtype=np.float64).reshape(n, 3)
     for r in range(world):
         assert np.array_equal(res[r], want)
+
+
+def test_stabilise_trace_cpu_matches_oracle(oracle):
+    from paper_2512_16609_b200.distributed import stabilise_trace
+
+    rng = np.random.default_rng(5)
+    tr = rng.random((97, 3))
+    for lam in (0.0, 0.3, 0.95):
+        got = stabilise_trace(torch.from_numpy(tr), lam).numpy()
+        assert np.array_equal(got, oracle.ema_trace(tr, lam))
+    carry = torch.tensor([0.5, 0.6, 0.7], dtype=torch.float64)
+    assert np.array_equal(stabilise_trace(torch.from_numpy(tr), 0.7, carry).numpy(),
+                          oracle.ema_trace(tr, 0.7, carry.numpy()))
+    # causal: smoothing a clip in two pieces with the carry equals smoothing it whole
+    whole = stabilise_trace(torch.from_numpy(tr), 0.8)
+    head = stabilise_trace(torch.from_numpy(tr[:40]), 0.8)
+    tail = stabilise_trace(torch.from_numpy(tr[40:]), 0.8, head[-1])
+    assert torch.equal(torch.cat([head, tail]), whole)
+
+
+def _stab_worker(rank, world, port, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2512_16609_b200.distributed import stabilise_trace
+
+        lo, hi = shard_range(n, rank, world)
+        rng = np.random.default_rng(11)
+        full = rng.random((n, 3))
+        trace = gather_airlight_trace(torch.from_numpy(full[lo:hi].copy()), n)
+        q.put((rank, stabilise_trace(trace, 0.9).numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_trace_stabilised_gloo(oracle):
+    """world_size 2: every rank ends with the same global smoothed trace, equal to the
+    restatement over the unsharded clip (the exchange the GPU ranks make over NCCL)."""
+    world, n = 2, 13
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stab_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = oracle.ema_trace(np.random.default_rng(11).random((n, 3)), 0.9)
+    for r in range(world):
+        assert np.array_equal(res[r], want)

@@ -1,0 +1,156 @@
+"""Multi-GPU product API and the opt-in airlight stabilisation, on the GPU.
+
+The lease has one B200, so "several devices" are several shards on device 0
+(devices=[0, 0, ...]): separate engines, streams and workspaces, the same sharding
+and dhz_allgather_airlight exchange as on an 8-GPU box.  Frames are independent
+(reference pipeline.py:257-260), so sharded results must be bit-identical to the
+single-device run.
+
+Stabilisation (``stabilise=lam``) is NOT reference behaviour; it is
+checked against its own CPU restatement (oracle.ema_trace + the oracle pipeline
+with the smoothed airlight substituted), with the image/video parity bars.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _frames(cfg="c3", n=7, w=192, h=112):
+    from paper_2512_16609_b200.synthetic import make_frames
+
+    return make_frames(cfg, frames=n, width=w, height=h, device="cuda")
+
+
+def _param_sets():
+    from paper_2512_16609_b200 import DehazeParams
+
+    return [DehazeParams(resize_to=None), DehazeParams(resize_to=None, white_balance=True),
+            DehazeParams(resize_to=(96, 64)), DehazeParams.for_image(guided_radius=9)]
+
+
+@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("pi", range(4))
+def test_dehaze_batch_sharded_equals_single(k, pi):
+    from paper_2512_16609_b200 import dehaze_batch
+
+    p = _param_sets()[pi]
+    f = _frames()
+    want, wair = dehaze_batch(f, p)
+    out, air = dehaze_batch(f, p, devices=[0] * k)
+    assert torch.equal(out, want) and torch.equal(air, wair)
+
+
+def test_more_devices_than_frames():
+    from paper_2512_16609_b200 import DehazeParams, dehaze_batch
+
+    p = DehazeParams(resize_to=None)
+    f = _frames(n=2)
+    want, wair = dehaze_batch(f, p)
+    out, air = dehaze_batch(f, p, devices=[0, 0, 0, 0])
+    assert torch.equal(out, want) and torch.equal(air, wair)
+
+
+def test_host_batch_sharded():
+    from paper_2512_16609_b200 import DehazeParams, dehaze_host_batch
+
+    p = DehazeParams(resize_to=None)
+    f = _frames(n=9).cpu().pin_memory()
+    want, wair = dehaze_host_batch(f, p, chunk=2)
+    out, air = dehaze_host_batch(f, p, chunk=2, devices=[0, 0])
+    assert torch.equal(out, want) and torch.equal(air, wair)
+
+
+def test_process_stream_devices(monkeypatch):
+    from paper_2512_16609_b200 import DehazeParams, pipeline, process_stream
+
+    monkeypatch.setattr(pipeline, "_PIPE_BATCH_BYTES", 2 * 3 * 192 * 112)  # 2-frame batches
+    p = DehazeParams(resize_to=None)
+    frames = list(_frames(n=11).cpu().numpy())
+    a, b = [], []
+    s1 = process_stream(frames, p, sink=a.append)
+    s2 = process_stream(frames, p, sink=b.append, devices=[0, 0])
+    assert all(np.array_equal(x, y) for x, y in zip(a, b)) and len(a) == len(b) == 11
+    assert all(np.array_equal(x, y) for x, y in zip(s1.airlight_trace, s2.airlight_trace))
+
+
+def test_ema_kernel_matches_restatement(oracle):
+    from paper_2512_16609_b200.engine import ema_airlight
+
+    rng = np.random.default_rng(3)
+    tr = rng.random((301, 3)) * 0.5 + 0.4
+    for lam in (0.0, 0.5, 0.9, 0.999):
+        got = ema_airlight(torch.from_numpy(tr).cuda(), lam).cpu().numpy()
+        assert np.array_equal(got, oracle.ema_trace(tr, lam))
+        carry = np.array([0.7, 0.8, 0.9])
+        got = ema_airlight(torch.from_numpy(tr).cuda(), lam, carry=torch.from_numpy(carry).cuda()).cpu().numpy()
+        assert np.array_equal(got, oracle.ema_trace(tr, lam, carry))
+    with pytest.raises(ValueError, match="stabilise"):
+        ema_airlight(torch.from_numpy(tr).cuda(), 1.0)
+
+
+def test_stabilise_zero_is_reference():
+    from paper_2512_16609_b200 import DehazeParams, dehaze_batch
+
+    p = DehazeParams(resize_to=None)
+    f = _frames()
+    assert all(torch.equal(x, y) for x, y in zip(dehaze_batch(f, p), dehaze_batch(f, p, stabilise=0.0)))
+
+
+@pytest.mark.parametrize("pi", range(4))
+def test_stabilised_vs_oracle(oracle, pi):
+    from paper_2512_16609_b200 import dehaze_batch
+
+    p = _param_sets()[pi]
+    f = _frames(n=5)
+    out, air = dehaze_batch(f, p, stabilise=0.8)
+    want, smooth = oracle.dehaze_stabilised(list(f.cpu().numpy()), p, 0.8)
+    assert np.array_equal(air.cpu().numpy(), smooth)
+    for i, w in enumerate(want):
+        d = np.abs(out[i].cpu().numpy().astype(np.int16) - w.astype(np.int16))
+        assert d.max() <= 1 and int((d > 0).sum()) <= 2, (i, int(d.max()), int((d > 0).sum()))
+
+
+def test_stabilised_paths_agree(monkeypatch):
+    """Batch, sharded batch, chunked host batch and pipelined stream give the same
+    smoothed trace and bytes (the recurrence carries A' across chunks / batches)."""
+    from paper_2512_16609_b200 import DehazeParams, dehaze_batch, dehaze_host_batch, pipeline, process_stream
+
+    monkeypatch.setattr(pipeline, "_PIPE_BATCH_BYTES", 3 * 3 * 192 * 112)  # 3-frame batches
+    p = DehazeParams(resize_to=None)
+    f = _frames(n=10)
+    want, wair = dehaze_batch(f, p, stabilise=0.9)
+    out, air = dehaze_batch(f, p, stabilise=0.9, devices=[0, 0, 0])
+    assert torch.equal(out, want) and torch.equal(air, wair)
+    ho, ha = dehaze_host_batch(f.cpu().pin_memory(), p, chunk=4, stabilise=0.9)
+    assert torch.equal(ho, want.cpu()) and torch.equal(ha, wair.cpu())
+    ho, ha = dehaze_host_batch(f.cpu().pin_memory(), p, chunk=4, stabilise=0.9, devices=[0, 0])
+    assert torch.equal(ho, want.cpu()) and torch.equal(ha, wair.cpu())
+    got = []
+    st = process_stream(list(f.cpu().numpy()), p, sink=got.append, stabilise=0.9, devices=[0, 0])
+    assert all(np.array_equal(g, w) for g, w in zip(got, want.cpu().numpy()))
+    assert np.array_equal(np.array(st.airlight_trace), wair.cpu().numpy())
+
+
+def test_allgather_direct():
+    from paper_2512_16609_b200.engine import DeviceGroup
+
+    g = DeviceGroup([0, 0, 0])
+    blocks = [torch.arange(3 * c, dtype=torch.float64, device="cuda").reshape(c, 3) + 100 * i
+              for i, c in enumerate([2, 0, 3])]
+    recv = g.allgather_airlight(blocks, [2, 0, 3])
+    torch.cuda.synchronize()
+    want = torch.cat(blocks)
+    assert all(torch.equal(r, want) for r in recv)
+
+
+def test_argument_errors():
+    from paper_2512_16609_b200 import DehazeParams, dehaze_batch
+
+    f = _frames(n=2)
+    with pytest.raises(ValueError, match="stabilise"):
+        dehaze_batch(f, DehazeParams(resize_to=None), stabilise=1.5)
+    with pytest.raises(ValueError, match="CUDA"):
+        dehaze_batch(f, DehazeParams(resize_to=None), devices=["cpu"])
