@@ -62,14 +62,17 @@ def _size_note(params):
 def _base(cfg):
     """Synthetic frame config behind a bench config ("c3d" runs on the C3 frames)."""
     return cfg[:2]
-# algorithmic HBM bytes per pixel (SURVEY.md §8(d)): dark 4 + select 1 + recover 6 (+3 balance);
-# image mode: dark 4 + select 1 + guided pass 1 (read I 3, write a,b 16) + pass 2 (read a,b 16,
-# read I 3, write O 3) = 46, + balance (pass 2 writes t~ 8, apply reads I 3 + t~ 8, writes O 3) = 62
-ALG_BYTES = {"c1": 11, "c3": 11, "c4": 14, "c2": 62, "c5": 62,
+# algorithmic HBM bytes per pixel, SURVEY.md §8(d): dark 4 + select 1 + recover 6 (+3 balance);
+# image mode + balance 29 (dark 4 + select 1 + guided 7 (read I 3, write t~ fp32 4) + recover 6
+# + t~ read 4 + balance 3 + 4).  The strip kernels' own design moves more (pass 1 writes a, b
+# 16 B/px, pass 2 reads them, t~ is fp64): DESIGN_BYTES, reported beside it.
+ALG_BYTES = {"c1": 11, "c3": 11, "c4": 14, "c2": 29, "c5": 29,
              # resize path per INPUT pixel (1080p -> 640x480, 0.148 output px per input px): dark pass
              # reads I 3 + writes dark 8*0.148, select reads dark 8*0.148, recover reads I 3 + writes 3*0.148
              "c3d": round(6 + 19 * (640 * 480) / (1920 * 1080), 2)}
-GUIDED_BYTES = {False: 41, True: 57}
+DESIGN_BYTES = {"c2": 62, "c5": 62}
+# the guided stage (guided filter + recovery [+ balance]) at §8(d) bytes: 29 - dark 4 - select 1
+GUIDED_BYTES = {False: 13, True: 24}
 
 
 def _guided_chunk(n, H, W, params):
@@ -221,6 +224,33 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _count_launches(fn, stream):
+    """Kernels of this package launched by one call of ``fn`` (CUDA-graph replays included),
+    from a torch.profiler (CUPTI) trace; (None, None) if the profiler is unavailable."""
+    import torch
+
+    try:
+        from torch.profiler import ProfilerActivity, profile
+
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        names = {}
+        for ev in prof.events():
+            nm = ev.name or ""
+            if "dhz::" in nm or nm.startswith("_ZN3dhz") or "k_ema" in nm:
+                import re
+
+                m = re.search(r"(k_\w+)", nm)
+                key = m.group(1) if m else nm[:60]
+                names[key] = names.get(key, 0) + 1
+        total = sum(names.values())
+        return (total if total else None), names
+    except Exception:
+        return None, None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -282,7 +312,7 @@ def main():
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
 
     graph = None
-    if native and not args.no_graph:
+    if native and not args.no_graph and world == 1:
         # the batch pipeline captured once as a CUDA graph and replayed per step
         # (same kernels on the same buffers; removes the per-launch gaps)
         from paper_2512_16609_b200.engine import GraphedPipeline
@@ -296,6 +326,16 @@ def main():
 
     def step(ev=None):
         nonlocal out, air
+        if world > 1:
+            # the product's multi-GPU path: airlight half on this rank's shard, NCCL
+            # all-gather of the trace (24 B/frame), recovery half (distributed.dehaze_sharded)
+            from paper_2512_16609_b200.distributed import dehaze_sharded
+
+            out, _trace = dehaze_sharded(frames, params, n * world)
+            if ev is not None:
+                for e in ev:
+                    e.record(stream)
+            return
         if native and graph is not None and ev is None:
             graph.replay()
         elif native:
@@ -305,9 +345,6 @@ def main():
             if ev is not None:
                 for e in ev:
                     e.record(stream)
-        if world > 1:
-            from paper_2512_16609_b200.distributed import gather_airlight_trace
-            gather_airlight_trace(air, n * world)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -394,7 +431,8 @@ def main():
     elif native:
         gb = GUIDED_BYTES[params.balance_enabled()] * n * npx
         g_gbs = gb / (stage_ms[2] / 1000.0) / 1e9
-        roof = {"bound": "hbm", "kernel": "k_gf_pass1 + k_gf_pass2 (+k_gf_apply): fused guided filter + recovery",
+        roof = {"bound": "hbm", "kernel": "guided stage at SURVEY §8(d) bytes (%d B/px): k_gf_pass1 + k_gf_pass2 "
+                "(+ k_gf_thresholds + k_gf_apply)" % GUIDED_BYTES[params.balance_enabled()],
                 "achieved": round(g_gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(g_gbs / peak, 4),
                 "traffic": None, "peak_kind": peak_kind, "alg_bytes_per_launch": gb,
                 "launch_ms": round(stage_ms[2], 4)}
@@ -405,6 +443,12 @@ def main():
                 "peak": peak, "unit": "GB/s", "frac": round(pipe_gbs / peak, 4), "traffic": None,
                 "peak_kind": peak_kind, "alg_bytes_per_launch": pipe_bytes, "launch_ms": round(ms_step, 4)}
         launches = 24 * n
+
+    formula_launches = launches
+    launches, launch_names = _count_launches(lambda: step(None), stream)
+    launch_source = "counted: kernels of libdehaze_b200.so in one step under torch.profiler (CUPTI)"
+    if launches is None:
+        launches, launch_source = formula_launches, "formula (profiler unavailable)"
 
     # ---- e2e: host API with pinned buffers ----------------------------------
     e2e = None
@@ -431,6 +475,31 @@ def main():
                "ms_per_step": round(1000 * el, 3)}
         ok = torch.equal(host_out, out.cpu())
         e2e["matches_device_path"] = bool(ok)
+        # the reference's own entry point: process_stream over a list of numpy frames
+        # (pinned staging filled by the copy threads, fresh output arrays to the sink)
+        from paper_2512_16609_b200.pipeline import process_stream
+
+        frames_np = list(host_in.numpy())
+        got = []
+        process_stream(frames_np[: min(n, 8)], params, sink=got.append)   # warm-up
+        sk = 0
+
+        def sink(o):
+            nonlocal sk
+            sk += 1
+
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            st_ = process_stream(frames_np, params, sink=sink)
+        el_s = (time.perf_counter() - t0) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([el_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el_s = float(t.item())
+        e2e["process_stream"] = {"value": round(total_px / el_s / 1e6, 3), "unit": "MP/s",
+                                 "ms_per_step": round(1000 * el_s, 3),
+                                 "api": "process_stream(list of numpy frames, params, sink) (reference API)",
+                                 "frames_emitted": st_.frame_count}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -471,6 +540,9 @@ def main():
                                                                   "omega", "t_min", "gamma")}},
             "roofline": roof,
             "pipeline_roofline": {"alg_bytes_per_px": ALG_BYTES[cfg], "achieved": round(pipe_gbs, 1),
+                                  **({"design_bytes_per_px": DESIGN_BYTES[cfg],
+                                      "design_frac": round(DESIGN_BYTES[cfg] * n * npx / (ms_step / 1000.0) / 1e9
+                                                           / peak, 4)} if cfg in DESIGN_BYTES else {}),
                                   "frac": round(pipe_gbs / peak, 4),
                                   "stage_ms": {"dark(K1)": round(stage_ms[0], 4),
                                                "select+airlight(K2-K3)": round(stage_ms[1], 4),
@@ -479,6 +551,8 @@ def main():
                                                   {"lut(K5)": round(stage_ms[2], 4),
                                                    "recover(K6)": round(stage_ms[3], 4)})}},
             "gpu_launches": launches * args.steps,
+            "gpu_launches_source": launch_source,
+            "gpu_launches_per_step": launch_names,
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -497,6 +497,34 @@ def dehaze_host_batch(frames, params=None, out=None, airlight=None, chunk=None, 
 
 
 _STREAM_BATCH_BYTES = 256 << 20   # float path: ~256 MiB of input frames per device launch
+_COPY_THREADS = max(1, min(8, (__import__("os").cpu_count() or 1)))
+_copy_pool = None
+
+
+def _pool():
+    """Host-copy threads of process_stream (numpy/torch copies release the GIL)."""
+    global _copy_pool
+    if _copy_pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _copy_pool = ThreadPoolExecutor(max_workers=_COPY_THREADS, thread_name_prefix="dhz-copy")
+    return _copy_pool
+
+
+def _par_copy(dst, src):
+    """dst.copy_(src) for host tensors, split over the copy threads when large; returns
+    when the copy is complete."""
+    nb = src.numel() * src.element_size()
+    # measured on the B200 box's host (tools/stream_copy_probe.py): splitting a 6 MB 1080p
+    # frame over threads loses to one memcpy (dispatch cost); 4K/8K frames gain
+    k = min(_COPY_THREADS, nb >> 22) if nb >= (8 << 20) else 1  # >= 4 MiB per piece
+    if k < 2:
+        dst.copy_(src)
+        return
+    d, s_ = dst.reshape(-1), src.reshape(-1)
+    n = d.numel()
+    cuts = [n * i // k for i in range(k + 1)]
+    list(_pool().map(lambda i: d[cuts[i]:cuts[i + 1]].copy_(s_[cuts[i]:cuts[i + 1]]), range(k)))
 _STREAM_BATCH_MAX = 256
 _PIPE_BATCH_BYTES = 48 << 20      # native path: input bytes per pipelined batch
 _PIPE_SLOTS = 3
@@ -564,7 +592,7 @@ class _StreamPipe:
     def put(self, frame, emit):
         import torch
 
-        self.next_input(emit).copy_(torch.from_numpy(frame))
+        _par_copy(self.next_input(emit), torch.from_numpy(frame))  # done before the source reuses its buffer
         self.commit(emit)
 
     def submit(self):
@@ -599,13 +627,18 @@ class _StreamPipe:
         if not m:
             return
         self.events[s].synchronize()
-        for i in range(m):
-            if self.fresh:
-                out = np.empty(self.out_shape, dtype=np.uint8)   # the sink may keep it: a fresh array
-                torch.from_numpy(out).copy_(self.hout[s][i])
+        if self.fresh:  # the sink may keep them: fresh arrays, filled by the copy threads
+            outs = [np.empty(self.out_shape, dtype=np.uint8) for _ in range(m)]
+            hout = self.hout[s]
+            if m > 1 and outs[0].nbytes >= (1 << 19):
+                list(_pool().map(lambda i: torch.from_numpy(outs[i]).copy_(hout[i]), range(m)))
             else:
-                out = self.hout[s][i].numpy()
-            emit(out, self.hair[s][i].numpy().copy())
+                for i in range(m):
+                    torch.from_numpy(outs[i]).copy_(hout[i])
+        else:
+            outs = [self.hout[s][i].numpy() for i in range(m)]
+        for i in range(m):
+            emit(outs[i], self.hair[s][i].numpy().copy())
         self.inflight[s] = 0
 
     def finish(self, emit):

@@ -154,3 +154,31 @@ def test_argument_errors():
         dehaze_batch(f, DehazeParams(resize_to=None), stabilise=1.5)
     with pytest.raises(ValueError, match="CUDA"):
         dehaze_batch(f, DehazeParams(resize_to=None), devices=["cpu"])
+
+
+def test_dehaze_sharded_world1_nccl():
+    """distributed.dehaze_sharded (the torchrun path of bench.py --gpus N) in a world of one
+    NCCL rank: same bytes and trace as dehaze_batch."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2512_16609_b200 import DehazeParams, dehaze_batch
+    from paper_2512_16609_b200.distributed import dehaze_sharded
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        p = DehazeParams(resize_to=None)
+        f = _frames(n=6)
+        want, wair = dehaze_batch(f, p)
+        out, trace = dehaze_sharded(f, p, 6)
+        assert torch.equal(out, want) and torch.equal(trace, wair)
+        out, trace = dehaze_sharded(f, p, 6, stabilise=0.9)
+        w2, a2 = dehaze_batch(f, p, stabilise=0.9)
+        assert torch.equal(out, w2) and torch.equal(trace, a2)
+    finally:
+        dist.destroy_process_group()
