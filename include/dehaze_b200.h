@@ -176,6 +176,11 @@ int dhz_resize_bilinear_u8(const uint8_t* in, int h, int w, int height, int widt
 int dhz_channel_min_f64(const double* img, int64_t npx, double* out, void* stream);
 /* morphology.py:63-73 min_filter (radius >= 1; tmp: H*W doubles) */
 int dhz_min_filter_f64(const double* m, int height, int width, int radius, double* out, double* tmp, void* stream);
+/* morphology.py:76-92 min_filter_naive / estimation.py:128-141 box_filter_naive: the
+ * reference's per-pixel correctness references, as direct window scans (independent
+ * of the separable kernels; radius >= 1) */
+int dhz_min_filter_naive_f64(const double* m, int height, int width, int radius, double* out, void* stream);
+int dhz_box_filter_naive_f64(const double* m, int height, int width, int radius, double* out, void* stream);
 /* estimation.py:110-125 box_filter (radius >= 1; tmp: H*W doubles) */
 int dhz_box_filter_f64(const double* m, int height, int width, int radius, double* out, double* tmp, void* stream);
 /* estimation.py:144-172 guided_filter; floor_t > 0 also applies pipeline.py:203

@@ -88,6 +88,8 @@ SIGNATURES = {
     "dhz_resize_bilinear_u8": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_void_p, _c_void_p]),
     "dhz_channel_min_f64": (_c_int, [_c_void_p, _c_i64, _c_void_p, _c_void_p]),
     "dhz_min_filter_f64": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_void_p, _c_void_p]),
+    "dhz_min_filter_naive_f64": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_void_p]),
+    "dhz_box_filter_naive_f64": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_void_p]),
     "dhz_box_filter_f64": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_void_p, _c_void_p]),
     "dhz_guided_filter_f64": (_c_int, [_c_void_p, _c_void_p, _c_int, _c_int, _c_int, ctypes.c_double,
                                        ctypes.c_double, _c_void_p, _c_void_p, _c_void_p]),

@@ -125,6 +125,37 @@ __global__ void k_resize(const Src* __restrict__ in, int h, int w, int height, i
   }
 }
 
+// Direct-window oracles of the reference's correctness references, independent of
+// the separable kernels above: every output scans its own (2r+1)^2 window of the
+// edge-padded map.  morphology.py:76-92 (min; exact in any order) and
+// estimation.py:128-141 (window mean: a row-major sequential sum / k^2 here, numpy
+// sums pairwise; the reference tests compare with a 1e-6 tolerance).
+__global__ void k_min_naive(const double* __restrict__ m, int H, int W, int r, double* __restrict__ out) {
+  const int64_t n = (int64_t)H * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / W), x = (int)(i - (int64_t)y * W);
+    double v = m[i];
+    for (int dy = -r; dy <= r; ++dy) {
+      const double* row = m + (int64_t)min(max(y + dy, 0), H - 1) * W;
+      for (int dx = -r; dx <= r; ++dx) v = fmin(v, row[min(max(x + dx, 0), W - 1)]);
+    }
+    out[i] = v;
+  }
+}
+
+__global__ void k_box_naive(const double* __restrict__ m, int H, int W, int r, double kk, double* __restrict__ out) {
+  const int64_t n = (int64_t)H * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / W), x = (int)(i - (int64_t)y * W);
+    double s = 0.0;
+    for (int dy = -r; dy <= r; ++dy) {
+      const double* row = m + (int64_t)min(max(y + dy, 0), H - 1) * W;
+      for (int dx = -r; dx <= r; ++dx) s = __dadd_rn(s, row[min(max(x + dx, 0), W - 1)]);
+    }
+    out[i] = __ddiv_rn(s, kk);
+  }
+}
+
 // ----------------------------------------------------------- min filter ----
 __global__ void k_min_rows(const double* __restrict__ m, int H, int W, int r, double* __restrict__ out) {
   const int64_t n = (int64_t)H * W;
@@ -440,6 +471,15 @@ int dhz_resize_bilinear_u8(const uint8_t* in, int h, int w, int height, int widt
   k_resize<uint8_t><<<grid_for((int64_t)height * width * 3), kT, 0, S(stream)>>>(in, h, w, height, width, sy, sx,
                                                                                  out);
   return ret("resize_bilinear_u8");
+}
+int dhz_min_filter_naive_f64(const double* m, int H, int W, int r, double* out, void* stream) {
+  k_min_naive<<<grid_for((int64_t)H * W), kT, 0, S(stream)>>>(m, H, W, r, out);
+  return ret("min_filter_naive_f64");
+}
+int dhz_box_filter_naive_f64(const double* m, int H, int W, int r, double* out, void* stream) {
+  const double k = 2.0 * r + 1.0;
+  k_box_naive<<<grid_for((int64_t)H * W), kT, 0, S(stream)>>>(m, H, W, r, k * k, out);
+  return ret("box_filter_naive_f64");
 }
 int dhz_min_filter_f64(const double* m, int H, int W, int r, double* out, double* tmp, void* stream) {
   const int64_t n = (int64_t)H * W;

@@ -92,9 +92,12 @@ def box_filter(m, radius):
 
 
 def box_filter_naive(m, radius):
-    """Correctness reference in the reference package (estimation.py:128-141); the
-    device box filter serves both names here."""
-    return box_filter(m, radius)
+    """Per-pixel window mean (reference estimation.py:128-141): an independent device kernel
+    (each output sums its own edge-padded window), the reference's correctness check of
+    box_filter."""
+    t = fp.check_scalar_map(m)
+    r = check_radius(radius)
+    return _out(fp.box_filter_naive(t, r), m)
 
 
 def guided_filter(p, guide, radius=DEFAULT_GUIDED_RADIUS, eps=DEFAULT_GUIDED_EPS):

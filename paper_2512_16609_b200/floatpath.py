@@ -150,6 +150,24 @@ def box_filter(m_t, radius):
     return out
 
 
+def min_filter_naive(m_t, radius):
+    if radius == 0:
+        return m_t.clone()
+    h, w = m_t.shape
+    out = torch.empty_like(m_t)
+    _call("dhz_min_filter_naive_f64", m_t.data_ptr(), h, w, int(radius), out.data_ptr(), _stream())
+    return out
+
+
+def box_filter_naive(m_t, radius):
+    if radius == 0:
+        return m_t.clone()
+    h, w = m_t.shape
+    out = torch.empty_like(m_t)
+    _call("dhz_box_filter_naive_f64", m_t.data_ptr(), h, w, int(radius), out.data_ptr(), _stream())
+    return out
+
+
 def guided_filter(p_t, g_t, radius, eps, floor_t=0.0):
     h, w = p_t.shape
     out = torch.empty_like(p_t)

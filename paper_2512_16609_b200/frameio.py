@@ -66,7 +66,11 @@ def _fill(stream, view):
     readinto = getattr(stream, "readinto", None)
     while got < n:
         if readinto is not None:
-            k = readinto(view[got:])
+            try:
+                k = readinto(view[got:])
+            except NotImplementedError:  # e.g. an io.RawIOBase that only overrides read()
+                readinto = None
+                continue
             k = 0 if k is None else k
         else:
             chunk = stream.read(n - got)

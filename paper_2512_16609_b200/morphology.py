@@ -25,5 +25,9 @@ def min_filter(m, radius):
 
 
 def min_filter_naive(m, radius):
-    """Correctness reference name of the reference package; same device kernel."""
-    return min_filter(m, radius)
+    """Per-pixel window scan (reference morphology.py:76-92): an independent device kernel
+    (every output scans its own clamped window), the reference's correctness check of
+    min_filter."""
+    t = fp.check_scalar_map(m)
+    r = check_radius(radius)
+    return _out(fp.min_filter_naive(t, r), m)

@@ -101,3 +101,23 @@ def test_process_stream_flushes_before_a_failing_source():
         process_stream(read_raw_frames(io.BytesIO(raw), StreamHeader(width=64, height=32)),
                        DehazeParams(resize_to=None), sink=got.append)
     assert len(got) == 5
+
+
+def test_raw_reader_stream_with_only_read():
+    """An io.RawIOBase subclass overriding only read() (its readinto raises
+    NotImplementedError) in 5-byte dribbles: frames still reassemble
+    (reference tests/test_frameio.py TestRawStream, chunked reads)."""
+    import io
+
+    from paper_2512_16609_b200.frameio import StreamHeader, read_raw_frames
+
+    class Dribble(io.RawIOBase):
+        def __init__(self, data):
+            self._buf = io.BytesIO(data)
+
+        def read(self, n):
+            return self._buf.read(min(n, 5))
+
+    frame = np.arange(36, dtype=np.uint8).reshape(3, 4, 3)
+    out = list(read_raw_frames(Dribble(frame.tobytes()), StreamHeader(width=4, height=3)))
+    assert len(out) == 1 and np.array_equal(out[0], frame)
