@@ -90,6 +90,19 @@ def _ncu_traffic_per_px():
         return {}
 
 
+def _calibration(cfg):
+    """Real reference vs the oracle port on identical frames (tools/calibrate_cpu_baseline.py, run
+    where /root/reference exists; one thread each): how much slower the reference itself is."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_cpu_baseline_calibration.json")) as fh:
+            d = json.load(fh).get(_base(cfg))
+        return {"reference_time_over_port": d["port_over_reference"], "identical_outputs": d["identical_outputs"],
+                "source": "profiles/r02_cpu_baseline_calibration.json (survey container, 1 thread, "
+                          f"{d['frames']} {_base(cfg)} frames)"}
+    except Exception:
+        return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -218,7 +231,7 @@ def run_reference(args):
                    "frames_per_step": sample},
         "cpu_baseline": {"value": round(value, 3), "unit": "MP/s", "cores": workers, "kind": "port",
                          "sample": f"{sample} frames per step, oracle/dehaze_oracle.py process_stream "
-                                   f"workers={workers}"},
+                                   f"workers={workers}", "calibration": _calibration(cfg)},
         "e2e": {"value": round(value, 3), "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -508,7 +521,7 @@ def main():
         v, done, el = cpu_baseline(frames[:sample].cpu().numpy(), params, workers)
         cpu = {"value": round(v, 3), "unit": "MP/s", "cores": workers, "kind": "port",
                "sample": f"{done} frames of the {cfg} workload ({W}x{H}) through oracle/dehaze_oracle.py "
-                         f"process_stream(workers={workers}) in {el:.1f} s"}
+                         f"process_stream(workers={workers}) in {el:.1f} s", "calibration": _calibration(cfg)}
 
     if rank == 0:
         line = {
