@@ -1,6 +1,7 @@
 // C ABI of libdehaze_b200.so (see include/dehaze_b200.h).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cstdarg>
 #include <string>
@@ -14,6 +15,14 @@ thread_local std::string g_err;
 }  // namespace
 
 namespace dhz {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("DHZ_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 int abi_fail(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;

@@ -240,6 +240,7 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
     for (int sh = 16; sh > 0; sh >>= 1) um = max(um, __shfl_xor_sync(0xffffffffu, um, sh));
     if (lane == 0 && um) atomicMax(frame_max + f, um);
   }
+  pdl_trigger();  // the select chain (PDL) may start launching
 }
 
 template <int R>

@@ -92,6 +92,15 @@ __device__ __forceinline__ uint32_t max3u(uint32_t a, uint32_t b, uint32_t c) { 
 // pair starting one pixel later: (a.hi, b.lo)
 __device__ __forceinline__ uint32_t shift1(uint32_t a, uint32_t b) { return __funnelshift_r(a, b, 16); }
 
+// Programmatic dependent launch (PDL): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its predecessor
+// drains; pdl_wait() (griddepcontrol.wait) blocks until every prerequisite grid has
+// completed and its memory is visible (a no-op without the attribute), so it goes
+// before the first access of predecessor data.  pdl_trigger() lets the dependent grid
+// launch early (its CTAs then wait in pdl_wait); results never depend on where it sits.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint4 ldg_v4(const void* p) {
   return __ldg(reinterpret_cast<const uint4*>(p));
 }

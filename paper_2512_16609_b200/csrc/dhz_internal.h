@@ -5,7 +5,30 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <utility>
+
 namespace dhz {
+
+// Kernel launch with programmatic dependent launch (PDL) on the same stream: the
+// kernel may begin launching while the previous kernel drains (it must call
+// pdl_wait() before touching predecessor data).  pdl = false: a plain launch.
+bool pdl_enabled();  // DHZ_PDL=0 turns programmatic dependent launch off (A/B measurements)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // Set the thread-local message returned by dhz_last_error(); return `code`.
 int abi_fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));

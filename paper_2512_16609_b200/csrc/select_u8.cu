@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(kT)
 k_level_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int n, int H, int W,
              const uint32_t* __restrict__ frame_max, const uint32_t* __restrict__ unit_max,
              uint32_t* __restrict__ row_hist /* [n][H][16] */, uint32_t* __restrict__ frame_hist /* [n][16] */) {
+  pdl_wait();  // K1 (dark map, unit maxima) complete
   __shared__ uint32_t cnt[kWarps][kBandH * kCntPitch];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nb = (H + kBandH - 1) / kBandH, nu = (W + kUnitW - 1) / kUnitW;
@@ -132,6 +133,7 @@ k_level_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int n, int H, in
                            frame_hist, lane);
     }
   }
+  pdl_trigger();  // after the work: K3 must not take K2 slots
 }
 
 // ---------------------------------------------------------------------------
@@ -165,6 +167,7 @@ __global__ void __launch_bounds__(kT)
 k_threshold(int64_t npx, int64_t K, int H, const uint32_t* __restrict__ frame_max,
             const uint32_t* __restrict__ row_hist, const uint32_t* __restrict__ frame_hist,
             FrameSel* __restrict__ sel, uint32_t* __restrict__ full_list, uint32_t* __restrict__ row_info) {
+  pdl_wait();
   const int f = blockIdx.x;
   __shared__ int js_s;
   if (threadIdx.x < 32) {  // warp 0: inclusive scan of the kWin level counts from the top
@@ -229,6 +232,7 @@ template <bool VEC>
 __global__ void __launch_bounds__(kT)
 k_full_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_t K, FrameSel* __restrict__ sel,
             const uint32_t* __restrict__ full_list, uint32_t* __restrict__ hist256) {
+  pdl_wait();
   const uint32_t count = __ldcg(full_list);
   __shared__ uint32_t h[kWarps][256];
   __shared__ bool last;
@@ -285,6 +289,7 @@ k_full_hist(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int6
 __global__ void __launch_bounds__(kT)
 k_full_rows(const uint8_t* __restrict__ dark, int64_t dark_fs, int H, int W, FrameSel* __restrict__ sel,
             const uint32_t* __restrict__ full_list, uint32_t* __restrict__ row_info) {
+  pdl_wait();
   const uint32_t count = __ldcg(full_list);
   __shared__ bool last;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, part = blockIdx.x;
@@ -440,6 +445,7 @@ __global__ void __launch_bounds__(kT)
 k_compact(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_t K, int H, int W,
           const FrameSel* __restrict__ sel, const uint32_t* __restrict__ row_info,
           const uint32_t* __restrict__ unit_max, uint32_t* __restrict__ sel_idx) {
+  pdl_wait();
   const int f = blockIdx.y, part = blockIdx.x;
   const uint32_t mode = sel[f].mode;
   uint32_t* out = sel_idx + (int64_t)f * K;
@@ -476,6 +482,7 @@ k_compact(const uint8_t* __restrict__ dark, int64_t dark_fs, int64_t npx, int64_
 __global__ void __launch_bounds__(kT)
 k_airlight(const uint8_t* __restrict__ in, int64_t in_fs, int64_t K, double alpha, const FrameSel* __restrict__ sel,
            const uint32_t* __restrict__ sel_idx, double* __restrict__ airlight) {
+  pdl_wait();
   const int f = blockIdx.x;
   airlight_sum(in + f * in_fs, sel_idx + (int64_t)f * K, K, sel[f].mode == kSelAll, alpha, airlight + 3 * f);
 }
@@ -493,22 +500,31 @@ cudaError_t select_u8(const uint8_t* dark, int64_t dark_fs, const uint8_t* in, i
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int g2 = (int)std::min<int64_t>((items + 32 * kWarps - 1) / (32 * kWarps), 8LL * sms);
-  if (vec) {
-    k_level_hist<true><<<g2, kT, 0, st>>>(dark, dark_fs, n, H, W, ws.frame_max, ws.unit_max, ws.row_hist,
-                                          ws.frame_hist);
-  } else {
-    k_level_hist<false><<<g2, kT, 0, st>>>(dark, dark_fs, n, H, W, ws.frame_max, ws.unit_max, ws.row_hist,
-                                           ws.frame_hist);
-  }
-  k_threshold<<<n, kT, 0, st>>>(npx, K, H, ws.frame_max, ws.row_hist, ws.frame_hist, ws.sel, ws.full_list,
-                                ws.row_info);
+  // at least ~4 units per warp slot: a single small frame's few hundred units are spread
+  // over many warps (each lane-group then holds few qualifying units; integer counts, so
+  // the split never changes a result); large batches are capped at 8 CTAs per SM
+  const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>((items + 4 * kWarps - 1) / (4 * kWarps), 8LL * sms));
+  // every kernel of the chain is launched programmatically dependent (PDL) on the one before
+  cudaError_t e;
+  if ((e = launch_k(vec ? k_level_hist<true> : k_level_hist<false>, g2, kT, 0, st, true, dark, dark_fs, n, H, W,
+                    (const uint32_t*)ws.frame_max, (const uint32_t*)ws.unit_max, ws.row_hist, ws.frame_hist)))
+    return e;
+  if ((e = launch_k(k_threshold, n, kT, 0, st, true, npx, K, H, (const uint32_t*)ws.frame_max,
+                    (const uint32_t*)ws.row_hist, (const uint32_t*)ws.frame_hist, ws.sel, ws.full_list, ws.row_info)))
+    return e;
   const dim3 cgrid(kCompactParts, n), fgrid(kFullParts, std::min(n, kFullFrames));
-  if (vec) k_full_hist<true><<<fgrid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.sel, ws.full_list, ws.hist256);
-  else k_full_hist<false><<<fgrid, kT, 0, st>>>(dark, dark_fs, npx, K, ws.sel, ws.full_list, ws.hist256);
-  k_full_rows<<<fgrid, kT, 0, st>>>(dark, dark_fs, H, W, ws.sel, ws.full_list, ws.row_info);
-  k_compact<<<cgrid, kT, 0, st>>>(dark, dark_fs, npx, K, H, W, ws.sel, ws.row_info, ws.unit_max, ws.sel_idx);
-  k_airlight<<<n, kT, 0, st>>>(in, in_fs, K, alpha, ws.sel, ws.sel_idx, airlight);
+  if ((e = launch_k(vec ? k_full_hist<true> : k_full_hist<false>, fgrid, kT, 0, st, true, dark, dark_fs, npx, K,
+                    ws.sel, (const uint32_t*)ws.full_list, ws.hist256)))
+    return e;
+  if ((e = launch_k(k_full_rows, fgrid, kT, 0, st, true, dark, dark_fs, H, W, ws.sel, (const uint32_t*)ws.full_list,
+                    ws.row_info)))
+    return e;
+  if ((e = launch_k(k_compact, cgrid, kT, 0, st, true, dark, dark_fs, npx, K, H, W, (const FrameSel*)ws.sel,
+                    (const uint32_t*)ws.row_info, (const uint32_t*)ws.unit_max, ws.sel_idx)))
+    return e;
+  if ((e = launch_k(k_airlight, n, kT, 0, st, true, in, in_fs, K, alpha, (const FrameSel*)ws.sel,
+                    (const uint32_t*)ws.sel_idx, airlight)))
+    return e;
   return cudaGetLastError();
 }
 
