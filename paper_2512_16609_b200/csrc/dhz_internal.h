@@ -88,10 +88,17 @@ cudaError_t guided_recover_u8(const uint8_t* in, int64_t in_fs, int n, int H, in
 constexpr int kFusedMaxRadius = 63;
 bool guided_fused_ok(int H, int W, int r);
 bool guided_use_fused(int H, int W, int r);
+int guided_path(int H, int W, int r);  // 0 strip kernels, 1 one-pass exact, 2 two-pass exact
 size_t guided_fused_ws_bytes(int n, int H, int W, int r, bool balance);
 cudaError_t guided_fused_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, int r, double eps,
                             const double* airlight, double omega, double t_min, const double* thr, double gamma,
                             bool balance, uint8_t* out, int64_t out_fs, void* ws, cudaStream_t st);
+// Two-pass form of the same exact filter (pass 1 writes the fixed-point a, b; pass 2
+// boxes them): the same bytes as guided_fused_u8.
+size_t guided_x_ws_bytes(int n, int H, int W, int r, bool balance);
+cudaError_t guided_x_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, int r, double eps,
+                        const double* airlight, double omega, double t_min, const double* thr, double gamma,
+                        bool balance, uint8_t* out, int64_t out_fs, void* ws, cudaStream_t st);
 // Gray-world apply: bytes from t~ (fp64 [n][npx]), airlight and per-frame channel
 // thresholds / gains (balance_thresholds below).
 cudaError_t guided_apply(const uint8_t* in, int64_t in_fs, int n, int64_t npx, const double* t,

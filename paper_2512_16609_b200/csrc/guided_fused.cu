@@ -71,6 +71,7 @@ struct FusedArgs {
   double* t_out;                  // MODE 1: t~ per pixel [n][H*W]
   unsigned long long* bsum;       // MODE 1: [n][3] fixed-point channel sums (2^38)
   long long* edge;                // [ctas][threads][16] a_q, b_q of rows 0 and H-1
+  longlong2* ab;                  // two-pass form: (a_q, b_q) per pixel [n][H*W]
 };
 
 struct FusedShared {
@@ -805,6 +806,595 @@ FusedPlan fused_plan(int n, int H, int W, int r, int sms) {
   return P;
 }
 
+
+// ---------------------------------------------------------------------------
+// Two-pass form of the same exact filter (the default for r <= kFusedMaxRadius).
+// Pass 1 (k_gx_ab) walks a column strip with the lead window only and writes every
+// pixel's fixed-point (a_q, b_q) — the very integers the one-pass kernel's lead
+// produces (same exact sums, same fp64 code in ab_from_sums) — 16 B/px.  Pass 2
+// (k_gx_out) walks a strip of (a_q, b_q) with vertical sliding sums (the leaving row
+// is read back instead of recomputed by a trail window) and forms t~ and the output
+// exactly as the one-pass kernel does, so both forms give the same bytes.  Compared
+// with the one-pass kernel this drops the trail's second horizontal scan and second
+// a/b evaluation (about half the instructions) and the per-thread private state in
+// shared memory (more warps per SM), for 16 B/px written and 32 B/px read back.
+// A pixel's a/b and output do not depend on the strip / segment / CTA split (exact
+// integer sums), so the segments are long and the split is by rows of the batch.
+constexpr int kXThreads = 256;            // 8 warps, 4 strip columns per thread
+constexpr int kXCols = 4 * kXThreads;     // strip columns (prefix window <= 2r+1 <= 127 < 128 per warp)
+constexpr int kXTw = kXThreads / 32 + 2;  // warp-total slots (+1: a window's second warp may be past the end; +1: even, keeps 16-B alignment)
+
+// Pass-1 shared memory: double-buffered (by row parity) prefixes of 3 words + warp totals.
+constexpr size_t kXSmem1 = 2ull * (3 * 8 * kXCols + 3 * 8 * kXTw);
+// Pass-2: double-buffered prefixes of the a, b column sums + warp totals, then the
+// cp.async staging of the next step's entering / leaving (a_q, b_q) (2 rows x 4 columns
+// x 16 B per thread, one stage: refilled right after it is consumed, so the loads have
+// the rest of the step in flight and hold no registers).
+constexpr size_t kXStage = 2ull * 4 * 16 * kXThreads;
+constexpr size_t kXSmem2 = 2ull * (2 * 8 * kXCols + 2 * 8 * kXTw) + kXStage;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// One Kogge-Stone step of a warp inclusive scan: x += (value of lane - o) for lanes
+// >= o, as a predicated add on the shuffle's own in-range predicate (no SELs).
+__device__ __forceinline__ uint64_t scan_step(uint64_t x, int o) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 l, h, xl, xh;\n\t.reg .b64 y;\n\t"
+      "mov.b64 {xl, xh}, %0;\n\t"
+      "shfl.sync.up.b32 l|p, xl, %1, 0, -1;\n\t"
+      "shfl.sync.up.b32 h, xh, %1, 0, -1;\n\t"
+      "mov.b64 y, {l, h};\n\t"
+      "@p add.u64 %0, %0, y;\n\t}"
+      : "+l"(x)
+      : "r"(o));
+  return x;
+}
+__device__ __forceinline__ uint32_t scan_step(uint32_t x, int o) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 y;\n\t"
+      "shfl.sync.up.b32 y|p, %0, %1, 0, -1;\n\t"
+      "@p add.u32 %0, %0, y;\n\t}"
+      : "+r"(x)
+      : "r"(o));
+  return x;
+}
+
+// Warp-local exclusive prefixes of 2 or 3 words (the thread's 4 columns each) with the
+// warp totals, the shuffle chains interleaved.
+template <typename U3>
+__device__ __forceinline__ void x_scan3(const uint64_t (&a)[4], const uint64_t (&b)[4], const U3 (&c)[4],
+                                        uint64_t* __restrict__ Ea, uint64_t* __restrict__ Eb, U3* __restrict__ Ec,
+                                        uint64_t* __restrict__ Ta, uint64_t* __restrict__ Tb, U3* __restrict__ Tc) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t a1 = a[0] + a[1], a2 = a1 + a[2], a3 = a2 + a[3];
+  const uint64_t b1 = b[0] + b[1], b2 = b1 + b[2], b3 = b2 + b[3];
+  const U3 c1 = c[0] + c[1], c2 = c1 + c[2], c3 = c2 + c[3];
+  uint64_t xa = a3, xb = b3;
+  U3 xc = c3;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    xa = scan_step(xa, o);
+    xb = scan_step(xb, o);
+    xc = scan_step(xc, o);
+  }
+  const uint64_t oa = xa - a3, ob = xb - b3;
+  const U3 oc = xc - c3;
+  const int k = 4 * threadIdx.x;
+  reinterpret_cast<ulonglong2*>(Ea + k)[0] = make_ulonglong2(oa, oa + a[0]);
+  reinterpret_cast<ulonglong2*>(Ea + k)[1] = make_ulonglong2(oa + a1, oa + a2);
+  reinterpret_cast<ulonglong2*>(Eb + k)[0] = make_ulonglong2(ob, ob + b[0]);
+  reinterpret_cast<ulonglong2*>(Eb + k)[1] = make_ulonglong2(ob + b1, ob + b2);
+  if (sizeof(U3) == 4) {
+    *reinterpret_cast<uint4*>(Ec + k) = make_uint4((uint32_t)oc, (uint32_t)(oc + c[0]), (uint32_t)(oc + c1),
+                                                   (uint32_t)(oc + c2));
+  } else {
+    reinterpret_cast<ulonglong2*>(Ec + k)[0] = make_ulonglong2((uint64_t)oc, (uint64_t)(oc + c[0]));
+    reinterpret_cast<ulonglong2*>(Ec + k)[1] = make_ulonglong2((uint64_t)(oc + c1), (uint64_t)(oc + c2));
+  }
+  if (lane == 31) {
+    Ta[threadIdx.x >> 5] = xa;
+    Tb[threadIdx.x >> 5] = xb;
+    Tc[threadIdx.x >> 5] = xc;
+  }
+}
+
+__device__ __forceinline__ void scan_store2(const uint64_t (&a)[4], const uint64_t (&b)[4], uint64_t* __restrict__ Ea,
+                                            uint64_t* __restrict__ Eb, uint64_t* __restrict__ Ta,
+                                            uint64_t* __restrict__ Tb) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t a1 = a[0] + a[1], a2 = a1 + a[2], a3 = a2 + a[3];
+  const uint64_t b1 = b[0] + b[1], b2 = b1 + b[2], b3 = b2 + b[3];
+  uint64_t xa = a3, xb = b3;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    xa = scan_step(xa, o);
+    xb = scan_step(xb, o);
+  }
+  const uint64_t oa = xa - a3, ob = xb - b3;
+  const int k = 4 * threadIdx.x;
+  reinterpret_cast<ulonglong2*>(Ea + k)[0] = make_ulonglong2(oa, oa + a[0]);
+  reinterpret_cast<ulonglong2*>(Ea + k)[1] = make_ulonglong2(oa + a1, oa + a2);
+  reinterpret_cast<ulonglong2*>(Eb + k)[0] = make_ulonglong2(ob, ob + b[0]);
+  reinterpret_cast<ulonglong2*>(Eb + k)[1] = make_ulonglong2(ob + b1, ob + b2);
+  if (lane == 31) {
+    Ta[threadIdx.x >> 5] = xa;
+    Tb[threadIdx.x >> 5] = xb;
+  }
+}
+
+// Per-segment frame constants of pass 1: m* (largest unclipped m) and c = omega/(255 max A).
+__device__ __forceinline__ bool x_frame_setup(const FusedArgs& A, FusedShared& S, int f, FrameConst& K) {
+  const double a0 = A.airlight[3 * f], a1 = A.airlight[3 * f + 1], a2 = A.airlight[3 * f + 2];
+  const double amax = fmax(fmax(a0, a1), a2);
+  if (threadIdx.x == 0) {
+    S.sA[0] = a0;
+    S.sA[1] = a1;
+    S.sA[2] = a2;
+    S.mstar = -1;
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < 256; m += blockDim.x) {
+    const double p = __dsub_rn(1.0, __dmul_rn(A.omega, __ddiv_rn(__ddiv_rn((double)m, 255.0), amax)));
+    if (p > A.t_min) atomicMax(&S.mstar, m);
+  }
+  __syncthreads();
+  K.cw = __ddiv_rn(A.omega, __dmul_rn(255.0, amax));
+  K.omt = __dsub_rn(1.0, A.t_min);
+  return S.mstar < 255;
+}
+
+// Strip geometry shared by both passes: output columns [xo0, xo1) of the frame, strip
+// column 0 at frame column xs (a multiple of 4, xs <= xo0 - r), the thread's 4 columns
+// at xs + 4t.  The plan keeps xo1 - 1 + r + 1 - xs <= kXCols - 1 (every output column's
+// window inside the strip's exclusive prefix).
+struct XGeo {
+  int xo0, xo1, xs, xt;
+  uint32_t outmask;
+  bool need;  // the thread holds a column some output window reads
+};
+
+__device__ __forceinline__ XGeo x_geo(const FusedArgs& A, int strip) {
+  XGeo g;
+  g.xo0 = strip * A.ow;
+  g.xo1 = min(A.W, g.xo0 + A.ow);
+  g.xs = (g.xo0 - A.r) & ~3;
+  g.xt = g.xs + 4 * (int)threadIdx.x;
+  g.outmask = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (g.xt + c >= g.xo0 && g.xt + c < g.xo1) g.outmask |= 1u << c;
+  g.need = g.xt < g.xo1 + A.r;
+  return g;
+}
+
+// Pass 1 over output rows [y0, y1) of one strip: (a_q, b_q) of every output pixel.
+template <bool CLIP, int R4>
+__device__ __forceinline__ void x_ab_segment(const FusedArgs& A, const FusedShared& S, unsigned char* dyn, int f,
+                                          int strip, int y0, int y1, const FrameConst K) {
+  using Q3T = typename Feat<CLIP>::Q3T;
+  constexpr int LOFF = (4 - R4) & 3, HOFF = (R4 + 1) & 3;
+  const int r = A.r, H = A.H, W = A.W;
+  const int t = threadIdx.x;
+  const XGeo G = x_geo(A, strip);
+  const uint8_t* frame = A.in + (int64_t)f * A.in_fs;
+  const int64_t pitch = 3LL * W;
+  const bool vec = G.xt >= 0 && G.xt + 3 < W && (W & 3) == 0 && ((uintptr_t)frame & 3) == 0;
+
+  // per row parity b: [e1 | e2 | e3 | warp totals (3 words)], kXBuf1 bytes
+  constexpr int kXBuf1 = 3 * 8 * kXCols + 3 * 8 * kXTw;
+  WinGeo g;
+  {
+    const int jo[4] = {4 * t, 4 * t + 1, 4 * t + 2, 4 * t + 3};
+    g = win_geo(jo, r, kXCols);
+  }
+  const uint32_t outmask = G.outmask & g.valid;
+#define CL(y) min(max((y), 0), H - 1)
+  Feat<CLIP> L;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    L.q1[c] = L.q2[c] = 0;
+    L.q3[c] = 0;
+  }
+  if (G.need) {  // warm-up: rows y0-r .. y0+r, four loads in flight
+    int y = y0 - r;
+    for (; y + 3 <= y0 + r; y += 4) {
+      uint32_t w[4][3];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load_row(w[u], frame, pitch, CL(y + u), G.xt, W, vec);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        Feat<CLIP> fe;
+        features<CLIP>(w[u], S.mstar, fe);
+        accumulate<CLIP>(L, &fe, nullptr);
+      }
+    }
+    for (; y <= y0 + r; ++y) {
+      uint32_t w[3];
+      load_row(w, frame, pitch, CL(y), G.xt, W, vec);
+      Feat<CLIP> fe;
+      features<CLIP>(w, S.mstar, fe);
+      accumulate<CLIP>(L, &fe, nullptr);
+    }
+  }
+  uint32_t nE[3] = {0, 0, 0}, nL[3] = {0, 0, 0};
+  if (G.need && y0 + 1 < y1) {
+    load_row(nE, frame, pitch, CL(y0 + r + 1), G.xt, W, vec);
+    load_row(nL, frame, pitch, CL(y0 - r), G.xt, W, vec);
+  }
+  longlong2* abf = A.ab + (int64_t)f * H * W;
+  for (int y = y0; y < y1; ++y) {
+    const int b = y & 1;
+    uint64_t* const e1 = reinterpret_cast<uint64_t*>(dyn + b * kXBuf1);
+    uint64_t* const e2 = e1 + kXCols;
+    Q3T* const e3 = reinterpret_cast<Q3T*>(e2 + kXCols);
+    uint64_t* const tw = e2 + 2 * kXCols;
+    x_scan3<Q3T>(L.q1, L.q2, L.q3, e1, e2, e3, tw, tw + kXTw, reinterpret_cast<Q3T*>(tw + 2 * kXTw));
+    if (G.need && y + 1 < y1) {  // slide the window one row down while the others scan
+      const uint32_t wE[3] = {nE[0], nE[1], nE[2]}, wL[3] = {nL[0], nL[1], nL[2]};
+      if (y + 2 < y1) {
+        load_row(nE, frame, pitch, CL(y + r + 2), G.xt, W, vec);
+        load_row(nL, frame, pitch, CL(y - r + 1), G.xt, W, vec);
+      }
+      Feat<CLIP> fe, fl;
+      features<CLIP>(wE, S.mstar, fe);
+      features<CLIP>(wL, S.mstar, fl);
+      accumulate<CLIP>(L, &fe, &fl);
+    }
+    __syncthreads();
+    if (outmask) {
+      uint64_t w1[4], w2[4];
+      Q3T w3[4];
+      window4<uint64_t, LOFF, HOFF>(e1, tw, g, 4 * t, 4 * t + 1, 4 * t + 2, 4 * t + 3, r, w1);
+      window4<uint64_t, LOFF, HOFF>(e2, tw + kXTw, g, 4 * t, 4 * t + 1, 4 * t + 2, 4 * t + 3, r, w2);
+      window4<Q3T, LOFF, HOFF>(e3, reinterpret_cast<Q3T*>(tw + 2 * kXTw), g, 4 * t, 4 * t + 1, 4 * t + 2,
+                               4 * t + 3, r, w3);
+      longlong2 v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        long long aq, bq;
+        ab_from_sums<CLIP>(w1[c], w2[c], (uint64_t)w3[c], A, K, aq, bq);
+        v[c] = make_longlong2(aq, bq);
+      }
+      longlong2* dst = abf + (int64_t)y * W + G.xt;
+      if (outmask == 15u) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dst[c] = v[c];
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (outmask >> c & 1) dst[c] = v[c];
+      }
+    }
+  }
+#undef CL
+}
+
+// Persistent CTAs over the flat (frame, strip) x rows space, as k_gf_fused.
+__global__ void __launch_bounds__(kXThreads, 2) k_gx_ab(FusedArgs A, int nframes) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ FusedShared S;
+  const int64_t cols = (int64_t)nframes * A.nstrips;
+  const int64_t total = cols * A.H;
+  const int64_t b0 = total * blockIdx.x / gridDim.x, b1 = total * (blockIdx.x + 1) / gridDim.x;
+  for (int64_t b = b0; b < b1;) {
+    const int64_t col = b / A.H;
+    const int yseg0 = (int)(b - col * A.H);
+    const int64_t end = min(b1, (col + 1) * A.H);
+    const int yseg1 = yseg0 + (int)(end - b);
+    b = end;
+    const int f = (int)(col / A.nstrips), strip = (int)(col - (int64_t)f * A.nstrips);
+    __syncthreads();  // the previous segment's readers of S / the prefixes are done
+    FrameConst K;
+    const bool clip = x_frame_setup(A, S, f, K);
+#define DHZ_SEG(R4)                                                             \
+  if (clip) x_ab_segment<true, R4>(A, S, dyn, f, strip, yseg0, yseg1, K);      \
+  else x_ab_segment<false, R4>(A, S, dyn, f, strip, yseg0, yseg1, K);
+    switch (A.r & 3) {
+      case 0: DHZ_SEG(0) break;
+      case 1: DHZ_SEG(1) break;
+      case 2: DHZ_SEG(2) break;
+      default: DHZ_SEG(3) break;
+    }
+#undef DHZ_SEG
+  }
+}
+
+__device__ __forceinline__ void load_ab4(longlong2 (&v)[4], const longlong2* __restrict__ row, int xt,
+                                         const int (&jc)[4], bool vec) {
+  if (vec) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = row[xt + c];
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = row[jc[c]];
+  }
+}
+
+// fp32 fast path of the output bytes (pass 2 without balance).  The exact byte of a
+// recovered sample x (fp64, from t~) is the k with thr[k] <= x < thr[k+1].  xf, the
+// same x in fp32 from a float copy of t~ (RN), its approximate reciprocal (rcp.approx,
+// rel. error < 2^-22) and dq = RN_f(RN(v/255) - A) (rel. 2^-24) with one FFMA,
+// satisfies |xf - x| <= |x - A| 2^-21.4 + 2^-24 < 4.6e-7 wherever |x - A| <= 1, i.e.
+// wherever a byte window's finite edge lies; the byte is accepted when xf lies in its
+// window shrunk by kXMargin = 1e-6 on both sides (float edges rounded inwards), and
+// recomputed exactly (fp64, Markstein division, the exact thresholds) otherwise.
+constexpr double kXMargin = 1e-6;
+struct XOutShared {
+  float2 win[256];      // (lo, hi) acceptance window of byte k
+  uint8_t guess[4104];  // byte of x = b / 4096, b <= 4096 (x >= 1) (the walk only goes up from it)
+  float dq[3][256];     // RN_f(RN(v / 255) - A_c) of the segment's frame
+  float af[3];
+};
+
+__device__ __forceinline__ void x_out_tables(XOutShared& X, const double* __restrict__ thr) {
+  for (int k = threadIdx.x; k < 256; k += blockDim.x) {
+    const float lo = k == 0 ? -INFINITY : __double2float_ru(__dadd_rn(thr[k], kXMargin));
+    const float hi = k == 255 ? INFINITY : __double2float_rd(__dsub_rn(thr[k + 1], kXMargin));
+    X.win[k] = make_float2(lo, hi);
+  }
+  for (int b = threadIdx.x; b <= 4096; b += blockDim.x) {
+    const double x = (double)b * (1.0 / 4096.0);
+    int lo = 0, hi = 255;  // largest k in [0, 255] with k == 0 or thr[k] <= x
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (thr[mid] <= x) lo = mid;
+      else hi = mid - 1;
+    }
+    X.guess[b] = (uint8_t)lo;
+  }
+}
+
+__device__ __forceinline__ uint32_t x_fast_byte(const XOutShared& X, float xf, bool& ok) {
+  const uint32_t b = min(__float2uint_rd(xf * 4096.0f), 4096u);  // (negative -> 0)
+  int k = X.guess[b];
+  float2 w = X.win[k];
+  while (xf >= w.y) w = X.win[++k];  // (win[255].y = +inf)
+  ok = ok && xf >= w.x;
+  return (uint32_t)k;
+}
+
+// Pass 2 over output rows [y0, y1) of one strip: box of (a_q, b_q) -> t~ -> output.
+template <int MODE, int R4>
+__device__ __forceinline__ void x_out_segment(const FusedArgs& A, const FusedShared& S, const XOutShared& X,
+                                              unsigned char* dyn, int f, int strip, int y0, int y1,
+                                              unsigned long long* __restrict__ bsum3) {
+  constexpr int LOFF = (4 - R4) & 3, HOFF = (R4 + 1) & 3;
+  const int r = A.r, H = A.H, W = A.W;
+  const int t = threadIdx.x;
+  const XGeo G = x_geo(A, strip);
+  const uint8_t* frame = A.in + (int64_t)f * A.in_fs;
+  const int64_t pitch = 3LL * W;
+  const longlong2* abf = A.ab + (int64_t)f * H * W;
+  int jc[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) jc[c] = min(max(G.xt + c, 0), W - 1);
+  const bool vec_ab = G.xt >= 0 && G.xt + 3 < W;
+
+  // per row parity b: [eA | eB | warp totals (2 words)], kXBuf2 bytes; then the staging
+  constexpr int kXBuf2 = 2 * 8 * kXCols + 2 * 8 * kXTw;
+  unsigned char* d = dyn + 2 * kXBuf2;
+  WinGeo g;
+  {
+    const int jo[4] = {4 * t, 4 * t + 1, 4 * t + 2, 4 * t + 3};
+    g = win_geo(jo, r, kXCols);
+  }
+  const uint32_t outmask = G.outmask & g.valid;
+  const bool vec_in = outmask == 15u && (W & 3) == 0 && ((uintptr_t)frame & 3) == 0;
+  const bool vec_out = outmask == 15u && (W & 3) == 0 && ((uintptr_t)A.out & 3) == 0 && (A.out_fs & 3) == 0;
+#define CL(y) min(max((y), 0), H - 1)
+  uint64_t SA[4] = {0, 0, 0, 0}, SB[4] = {0, 0, 0, 0};
+  if (G.need) {
+    int y = y0 - r;
+    for (; y + 1 <= y0 + r; y += 2) {
+      longlong2 v0[4], v1[4];
+      load_ab4(v0, abf + (int64_t)CL(y) * W, G.xt, jc, vec_ab);
+      load_ab4(v1, abf + (int64_t)CL(y + 1) * W, G.xt, jc, vec_ab);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        SA[c] += (uint64_t)v0[c].x + (uint64_t)v1[c].x;
+        SB[c] += (uint64_t)v0[c].y + (uint64_t)v1[c].y;
+      }
+    }
+    for (; y <= y0 + r; ++y) {
+      longlong2 v0[4];
+      load_ab4(v0, abf + (int64_t)CL(y) * W, G.xt, jc, vec_ab);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        SA[c] += (uint64_t)v0[c].x;
+        SB[c] += (uint64_t)v0[c].y;
+      }
+    }
+  }
+  // staging slots of this thread: [stage][row E/L][column] (16 B each), SoA over threads
+  // so a warp's 16-byte accesses are contiguous
+  longlong2* stg = reinterpret_cast<longlong2*>(d);
+  auto slot = [&](int row, int c) -> longlong2* { return stg + (row * 4 + c) * kXThreads + t; };
+  auto stage_rows = [&](int YE, int YL) {
+    const longlong2* rE = abf + (int64_t)YE * W;
+    const longlong2* rL = abf + (int64_t)YL * W;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int x = vec_ab ? G.xt + c : jc[c];
+      cp_async16(slot(0, c), rE + x);
+      cp_async16(slot(1, c), rL + x);
+    }
+    cp_async_commit();
+  };
+  uint32_t nC[3] = {0, 0, 0};
+  if (G.need && y0 + 1 < y1) stage_rows(CL(y0 + r + 1), CL(y0 - r));
+  if (outmask) load_row(nC, frame, pitch, y0, G.xt, W, vec_in);
+  const double A0 = S.sA[0], A1 = S.sA[1], A2 = S.sA[2];
+  unsigned long long bs0 = 0, bs1 = 0, bs2 = 0;
+  for (int y = y0; y < y1; ++y) {
+    const int b = y & 1;
+    uint64_t* const eA = reinterpret_cast<uint64_t*>(dyn + b * kXBuf2);
+    uint64_t* const eB = eA + kXCols;
+    uint64_t* const tw = eB + kXCols;
+    scan_store2(SA, SB, eA, eB, tw, tw + kXTw);
+    const uint32_t wC[3] = {nC[0], nC[1], nC[2]};
+    if (G.need && y + 1 < y1) {
+      cp_async_wait_all();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const longlong2 e = *slot(0, c), l = *slot(1, c);
+        SA[c] += (uint64_t)e.x - (uint64_t)l.x;
+        SB[c] += (uint64_t)e.y - (uint64_t)l.y;
+      }
+      if (y + 2 < y1) stage_rows(CL(y + r + 2), CL(y - r + 1));
+      if (outmask) load_row(nC, frame, pitch, y + 1, G.xt, W, vec_in);
+    }
+    __syncthreads();
+    if (!outmask) continue;
+    uint64_t ba[4], bb[4];
+    window4<uint64_t, LOFF, HOFF>(eA, tw, g, 4 * t, 4 * t + 1, 4 * t + 2, 4 * t + 3, r, ba);
+    window4<uint64_t, LOFF, HOFF>(eB, tw + kXTw, g, 4 * t, 4 * t + 1, 4 * t + 2, 4 * t + 3, r, bb);
+    uint32_t ob[12];
+    const int64_t pix0 = (int64_t)y * W + G.xt;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      ob[3 * c] = ob[3 * c + 1] = ob[3 * c + 2] = 0;
+      if (!(outmask >> c & 1)) continue;
+      uint32_t R, Gc, B;
+      rgb_of(wC, c, R, Gc, B);
+      const double mab = __dmul_rn(__ll2double_rn((long long)ba[c]), A.rqkk);
+      const double mbb = __dmul_rn(__ll2double_rn((long long)bb[c]), A.rqkk);
+      const double gg = guide_n(299u * R + 587u * Gc + 114u * B);
+      const double tt = fmin(fmax(__dadd_rn(__dmul_rn(mab, gg), mbb), A.t_min), 1.0);
+      if (MODE == 0) {
+        const float tf = __double2float_rn(tt);
+        float rtf;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rtf) : "f"(tf));
+        bool ok = true;
+        uint32_t k0 = x_fast_byte(X, __fmaf_rn(X.dq[0][R], rtf, X.af[0]), ok);
+        uint32_t k1 = x_fast_byte(X, __fmaf_rn(X.dq[1][Gc], rtf, X.af[1]), ok);
+        uint32_t k2 = x_fast_byte(X, __fmaf_rn(X.dq[2][B], rtf, X.af[2]), ok);
+        if (!ok) {  // near a byte boundary: the exact fp64 recovery and thresholds
+          const double rt = __drcp_rn(tt);
+          const double x0 = recover_raw(S.f255[R], A0, tt, rt), x1 = recover_raw(S.f255[Gc], A1, tt, rt),
+                       x2 = recover_raw(S.f255[B], A2, tt, rt);
+          k0 = quantize_pair(x0, S.thr2, (int)k0);
+          k1 = quantize_pair(x1, S.thr2, (int)k1);
+          k2 = quantize_pair(x2, S.thr2, (int)k2);
+        }
+        ob[3 * c] = k0;
+        ob[3 * c + 1] = k1;
+        ob[3 * c + 2] = k2;
+      } else {
+        A.t_out[(int64_t)f * H * W + pix0 + c] = tt;
+        const double rt = __drcp_rn(tt);
+        const double xv[3] = {recover_raw(S.f255[R], A0, tt, rt), recover_raw(S.f255[Gc], A1, tt, rt),
+                              recover_raw(S.f255[B], A2, tt, rt)};
+        unsigned long long q[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const double xc = fmin(fmax(xv[ch], 0.0), 1.0);
+          const double gv =
+              A.gamma_is_one ? xc : (A.pow_general ? pow(xc, A.inv_gamma) : pow_series(xc, A, S));
+          q[ch] = __double2ull_rn(__dmul_rn(gv, 0x1p38));  // exact fixed-point sums
+        }
+        bs0 += q[0];
+        bs1 += q[1];
+        bs2 += q[2];
+      }
+    }
+    if (MODE == 0) {
+      uint8_t* orow = A.out + (int64_t)f * A.out_fs + pix0 * 3;
+      if (vec_out) {
+        uint32_t* o32 = reinterpret_cast<uint32_t*>(orow);
+        o32[0] = ob[0] | (ob[1] << 8) | (ob[2] << 16) | (ob[3] << 24);
+        o32[1] = ob[4] | (ob[5] << 8) | (ob[6] << 16) | (ob[7] << 24);
+        o32[2] = ob[8] | (ob[9] << 8) | (ob[10] << 16) | (ob[11] << 24);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (outmask >> c & 1) {
+            orow[3 * c] = (uint8_t)ob[3 * c];
+            orow[3 * c + 1] = (uint8_t)ob[3 * c + 1];
+            orow[3 * c + 2] = (uint8_t)ob[3 * c + 2];
+          }
+      }
+    }
+  }
+#undef CL
+  if (MODE == 1) {  // per-frame channel sums (integer: order-free)
+    unsigned long long v[3] = {bs0, bs1, bs2};
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[ch] += __shfl_xor_sync(0xffffffffu, v[ch], o);
+      if ((threadIdx.x & 31) == 0 && v[ch]) atomicAdd(&bsum3[ch], v[ch]);
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kXThreads, 2) k_gx_out(FusedArgs A, int nframes) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ FusedShared S;
+  __shared__ XOutShared X;
+  if (MODE == 0) x_out_tables(X, A.thr);
+  const double e = A.inv_gamma;
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+    S.f255[v] = __ddiv_rn((double)v, 255.0);
+    S.thr2[v] = make_double2(v == 0 ? -INFINITY : A.thr[v], v == 255 ? INFINITY : A.thr[v + 1]);
+  }
+  if (MODE == 1 && !A.gamma_is_one) {
+    for (int j = threadIdx.x; j < 128; j += blockDim.x) {
+      const double c = 1.0 + ((double)j + 0.5) / 128.0;
+      S.pt_ce[j] = pow(c, e);
+      S.pt_ri[j] = __ddiv_rn(1.0, c);
+    }
+    for (int k = threadIdx.x; k <= 64; k += blockDim.x) S.pt_p2[k] = exp2(-(double)k * e);
+  }
+  const int64_t cols = (int64_t)nframes * A.nstrips;
+  const int64_t total = cols * A.H;
+  const int64_t b0 = total * blockIdx.x / gridDim.x, b1 = total * (blockIdx.x + 1) / gridDim.x;
+  for (int64_t b = b0; b < b1;) {
+    const int64_t col = b / A.H;
+    const int yseg0 = (int)(b - col * A.H);
+    const int64_t end = min(b1, (col + 1) * A.H);
+    const int yseg1 = yseg0 + (int)(end - b);
+    b = end;
+    const int f = (int)(col / A.nstrips), strip = (int)(col - (int64_t)f * A.nstrips);
+    __syncthreads();
+    if (threadIdx.x < 3) S.sA[threadIdx.x] = A.airlight[3 * f + threadIdx.x];
+    if (MODE == 0) {
+      for (int i = threadIdx.x; i < 768; i += blockDim.x) {
+        const int ch = i >> 8, v = i & 255;
+        const double ac = A.airlight[3 * f + ch];
+        X.dq[ch][v] = __double2float_rn(__dsub_rn(__ddiv_rn((double)v, 255.0), ac));
+        if (v == 0) X.af[ch] = __double2float_rn(ac);
+      }
+    }
+    __syncthreads();
+    switch (A.r & 3) {
+      case 0: x_out_segment<MODE, 0>(A, S, X, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
+      case 1: x_out_segment<MODE, 1>(A, S, X, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
+      case 2: x_out_segment<MODE, 2>(A, S, X, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
+      default: x_out_segment<MODE, 3>(A, S, X, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
+    }
+  }
+}
+
+struct XPlan {
+  int ow, nstrips, ctas;
+};
+
+XPlan x_plan(int n, int H, int W, int r, int sms) {
+  XPlan P{};
+  const int ow_max = (kXCols - 2 * r - 4) & ~3;
+  P.nstrips = (W + ow_max - 1) / ow_max;
+  P.ow = (((W + P.nstrips - 1) / P.nstrips) + 3) & ~3;
+  const int64_t rows = (int64_t)n * P.nstrips * H;
+  // a segment pays a (2r+1)-row warm-up: keep >= 2r+1 (and >= 16) output rows per CTA
+  const int64_t by_rows = std::max<int64_t>(1, rows / std::max(16, 2 * r + 1));
+  P.ctas = (int)std::min<int64_t>(2LL * sms, by_rows);
+  return P;
+}
+
 }  // namespace
 
 bool guided_fused_ok(int H, int W, int r) { return r >= 1 && r <= kFusedMaxRadius && W >= 1 && H >= 1; }
@@ -908,6 +1498,116 @@ cudaError_t guided_fused_u8(const uint8_t* in, int64_t in_fs, int n, int H, int 
     A.bsum = bsum;
     if ((e = cudaMemsetAsync(bsum, 0, 24ull * c, st)) != cudaSuccess) return e;
     k_gf_fused<1><<<P.ctas, P.threads, P.smem, st>>>(A, c);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    k_bsum_to_part<<<(3 * c + 255) / 256, 256, 0, st>>>(bsum, c, part);
+    if ((e = balance_thresholds(part, 1, c, npx, gamma, bthr, gains, st)) != cudaSuccess) return e;
+    if ((e = guided_apply(A.in, in_fs, c, npx, tmap, A.airlight, bthr, gains, gamma, A.out, out_fs, st)) !=
+        cudaSuccess)
+      return e;
+  }
+  return cudaGetLastError();
+}
+
+// ---- two-pass form ----
+// Frames per chunk so (a_q, b_q) (+ t~ with balance) stay within ~12 GB.
+static int x_chunk(int n, int H, int W, bool balance) {
+  const double per = (balance ? 24.0 : 16.0) * (double)H * W;
+  const int cap = (int)std::max(1.0, std::min((double)n, 12.0e9 / per));
+  const int chunks = (n + cap - 1) / cap;
+  return (n + chunks - 1) / chunks;
+}
+
+size_t guided_x_ws_bytes(int n, int H, int W, int r, bool balance) {
+  (void)r;
+  const int chunk = x_chunk(n, H, W, balance);
+  const int64_t npx = (int64_t)H * W;
+  size_t b = 16ull * npx * chunk;
+  if (balance)
+    b += 8ull * npx * chunk + 24ull * chunk + 24ull * chunk + 3 * 256 * 8ull * chunk + 16ull * chunk + 1024;
+  return b;
+}
+
+static void x_args(FusedArgs& A, int H, int W, int r, double eps, int64_t in_fs, double omega, double t_min,
+                   const double* thr, double gamma, int64_t out_fs) {
+  A.H = H;
+  A.W = W;
+  A.r = r;
+  A.in_fs = in_fs;
+  A.omega = omega;
+  A.t_min = t_min;
+  const uint64_t kk = (uint64_t)(2 * r + 1) * (uint64_t)(2 * r + 1);
+  A.kk = kk;
+  const double kn = (double)kk * 255000.0;
+  A.E = eps * kn * kn;
+  const double amax = 1.0 / (4.0 * std::sqrt(eps)) + 1.5;
+  int s = (int)std::floor(62.0 - std::log2((double)kk) - std::log2(amax));
+  s = std::max(8, std::min(s, 52));
+  A.qs = std::ldexp(1.0, s);
+  A.rqkk = std::ldexp(1.0, -s) / (double)kk;
+  A.rkk = 1.0 / (double)kk;
+  A.r255kk = 1.0 / kn;
+  A.thr = thr;
+  A.inv_gamma = 1.0 / gamma;
+  A.gamma_is_one = gamma == 1.0 ? 1 : 0;
+  A.pow_general = (A.inv_gamma > 16.0) ? 1 : 0;
+  double c = 1.0;
+  A.h[0] = 1.0;
+  for (int k = 1; k <= 8; ++k) {
+    c *= (A.inv_gamma - (k - 1)) / k;
+    A.h[k] = c;
+  }
+  A.out_fs = out_fs;
+}
+
+cudaError_t guided_x_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, int r, double eps,
+                        const double* airlight, double omega, double t_min, const double* thr, double gamma,
+                        bool balance, uint8_t* out, int64_t out_fs, void* ws, cudaStream_t st) {
+  if (!guided_fused_ok(H, W, r)) return cudaErrorInvalidValue;
+  const int64_t npx = (int64_t)H * W;
+  const int sms = sm_count();
+  const int chunk = x_chunk(n, H, W, balance);
+  FusedArgs A{};
+  x_args(A, H, W, r, eps, in_fs, omega, t_min, thr, gamma, out_fs);
+  A.ab = static_cast<longlong2*>(ws);
+  uint8_t* base = static_cast<uint8_t*>(ws) + 16ull * npx * chunk;
+  double* tmap = reinterpret_cast<double*>(base);
+  unsigned long long* bsum = reinterpret_cast<unsigned long long*>(base + 8ull * npx * chunk);
+  double* part = reinterpret_cast<double*>(bsum + 3 * chunk);
+  double* bthr = part + 3 * chunk;
+  float* gains = reinterpret_cast<float*>(bthr + 3 * 256 * chunk);
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_gx_ab, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kXSmem1)) != cudaSuccess)
+    return e;
+  // two CTAs per SM need the largest shared-memory carveout (the default picked 164 KB)
+  if ((e = cudaFuncSetAttribute(k_gx_ab, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(k_gx_out<0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(k_gx_out<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(k_gx_out<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kXSmem2)) !=
+      cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(k_gx_out<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kXSmem2)) !=
+      cudaSuccess)
+    return e;
+  for (int f0 = 0; f0 < n; f0 += chunk) {
+    const int c = std::min(chunk, n - f0);
+    const XPlan P = x_plan(c, H, W, r, sms);
+    A.ow = P.ow;
+    A.nstrips = P.nstrips;
+    A.in = in + (int64_t)f0 * in_fs;
+    A.out = out + (int64_t)f0 * out_fs;
+    A.airlight = airlight + 3 * f0;
+    k_gx_ab<<<P.ctas, kXThreads, kXSmem1, st>>>(A, c);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (!balance) {
+      k_gx_out<0><<<P.ctas, kXThreads, kXSmem2, st>>>(A, c);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      continue;
+    }
+    A.t_out = tmap;
+    A.bsum = bsum;
+    if ((e = cudaMemsetAsync(bsum, 0, 24ull * c, st)) != cudaSuccess) return e;
+    k_gx_out<1><<<P.ctas, kXThreads, kXSmem2, st>>>(A, c);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     k_bsum_to_part<<<(3 * c + 255) / 256, 256, 0, st>>>(bsum, c, part);
     if ((e = balance_thresholds(part, 1, c, npx, gamma, bthr, gains, st)) != cudaSuccess) return e;

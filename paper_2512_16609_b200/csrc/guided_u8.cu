@@ -509,21 +509,27 @@ cudaError_t guided_apply(const uint8_t* in, int64_t in_fs, int n, int64_t npx, c
   return cudaGetLastError();
 }
 
-// DHZ_GUIDED_PATH=fused|strip forces one image-mode implementation (tests, probes).
+// DHZ_GUIDED_PATH=fused|twopass|strip forces one image-mode implementation (tests, probes).
 static int guided_path_override() {
   const char* s = getenv("DHZ_GUIDED_PATH");
   if (!s) return 0;
   if (!strcmp(s, "fused")) return 1;
   if (!strcmp(s, "strip")) return 2;
+  if (!strcmp(s, "twopass")) return 3;
   return 0;
 }
 
-// The strip kernels stay the default: the one-pass exact kernel reads/writes ~10 B/px
-// instead of ~90 but is issue-bound and measured slower.
-bool guided_use_fused(int H, int W, int r) {
-  if (!guided_fused_ok(H, W, r)) return false;
-  return guided_path_override() == 1;
+// Which image-mode implementation runs: 0 strip kernels (below), 1 one-pass exact
+// (guided_fused.cu), 2 two-pass exact (guided_fused.cu, same bytes as 1).
+int guided_path(int H, int W, int r) {
+  const int o = guided_path_override();
+  if (!guided_fused_ok(H, W, r)) return 0;
+  if (o == 1) return 1;
+  if (o == 3) return 2;
+  return 0;
 }
+
+bool guided_use_fused(int H, int W, int r) { return guided_path(H, W, r) == 1; }
 
 // Frames per chunk so the fp64 a/b (+t~) scratch stays within ~4 GB.
 int guided_chunk(int n, int H, int W, bool balance) {
@@ -532,7 +538,11 @@ int guided_chunk(int n, int H, int W, bool balance) {
 }
 
 size_t guided_ws_bytes(int n, int H, int W, int r, bool balance) {
-  if (guided_use_fused(H, W, r)) return guided_fused_ws_bytes(n, H, W, r, balance);
+  switch (guided_path(H, W, r)) {
+    case 1: return guided_fused_ws_bytes(n, H, W, r, balance);
+    case 2: return guided_x_ws_bytes(n, H, W, r, balance);
+    default: break;
+  }
   const int64_t npx = (int64_t)H * W;
   const int c = guided_chunk(n, H, W, balance);
   size_t b = 16ull * npx * c;                                            // a, b
@@ -549,9 +559,14 @@ cudaError_t guided_recover_u8(const uint8_t* in, int64_t in_fs, int n, int H, in
                               const double* airlight, double omega, double t_min, const double* thr, double gamma,
                               bool balance, uint8_t* out, int64_t out_fs, void* ws, cudaStream_t st) {
   if (r < 1 || r > kGuidedMaxRadius) return cudaErrorInvalidValue;
-  if (guided_use_fused(H, W, r))
-    return guided_fused_u8(in, in_fs, n, H, W, r, eps, airlight, omega, t_min, thr, gamma, balance, out, out_fs, ws,
-                           st);
+  switch (guided_path(H, W, r)) {
+    case 1:
+      return guided_fused_u8(in, in_fs, n, H, W, r, eps, airlight, omega, t_min, thr, gamma, balance, out, out_fs,
+                             ws, st);
+    case 2:
+      return guided_x_u8(in, in_fs, n, H, W, r, eps, airlight, omega, t_min, thr, gamma, balance, out, out_fs, ws, st);
+    default: break;
+  }
   const int64_t npx = (int64_t)H * W;
   const int chunk = guided_chunk(n, H, W, balance);
   const double inv_g = 1.0 / gamma;

@@ -1,5 +1,6 @@
-"""The one-pass exact-integer guided filter (guided_fused.cu), selected with
-DHZ_GUIDED_PATH=fused (the strip kernels are the default).
+"""The exact-integer guided filter (guided_fused.cu) in both of its forms: one pass
+(DHZ_GUIDED_PATH=fused) and two passes (DHZ_GUIDED_PATH=twopass, pass 1 writing the
+fixed-point a, b), which must give the same bytes.
 
 Its box sums are exact integers, so its output must not depend on how the frame is
 cut into strips, segments and persistent CTAs (batch size, frame count): checked by
@@ -15,10 +16,10 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True)
-def fused_path(monkeypatch):
-    monkeypatch.setenv("DHZ_GUIDED_PATH", "fused")
-    yield
+@pytest.fixture(autouse=True, params=["fused", "twopass"])
+def fused_path(monkeypatch, request):
+    monkeypatch.setenv("DHZ_GUIDED_PATH", request.param)
+    yield request.param
 
 
 def _params(**kw):
@@ -91,3 +92,19 @@ def test_matches_strip_path(monkeypatch):
     assert torch.equal(air_f, air_s)
     d = (out_f.to(torch.int16) - out_s.to(torch.int16)).abs()
     assert int(d.max()) <= 1 and int((d > 0).sum()) <= 4
+
+
+@pytest.mark.parametrize("balance", [True, False])
+def test_two_forms_identical(monkeypatch, balance):
+    """One pass and two passes compute the same integers and the same fp64 code."""
+    from paper_2512_16609_b200 import dehaze_batch
+    from paper_2512_16609_b200.synthetic import make_frames
+
+    p = _params(patch_radius=15, guided_radius=60, white_balance=balance)
+    frames = make_frames("c5", frames=3, width=4100, height=700, device="cuda")
+    outs = {}
+    for path in ("fused", "twopass"):
+        monkeypatch.setenv("DHZ_GUIDED_PATH", path)
+        outs[path] = dehaze_batch(frames, p)
+    assert torch.equal(outs["fused"][0], outs["twopass"][0])
+    assert torch.equal(outs["fused"][1], outs["twopass"][1])

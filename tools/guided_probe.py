@@ -1,4 +1,4 @@
-"""Times the two image-mode implementations (DHZ_GUIDED_PATH=fused|strip) on C5 / C2
+"""Times the image-mode implementations (DHZ_GUIDED_PATH=strip|fused|twopass) on C5 / C2
 batches with CUDA events, and checks they agree with each other (<= 1 LSB)."""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -35,8 +35,8 @@ for name in sys.argv[1:] or ["c5", "c2"]:
         best = min(tot, key=lambda v: sum(v))
         res[path] = dict(ms_total=round(sum(best), 3), stage_ms=[round(v, 3) for v in best])
         outs[path] = out.clone()
-    if len(outs) == 2:
-        d = (outs["strip"].to(torch.int16) - outs["fused"].to(torch.int16)).abs()
-        res["diff_max"] = int(d.max())
-        res["diff_n"] = int((d > 0).sum())
+    ref = next(iter(outs))
+    for path in list(outs)[1:]:
+        d = (outs[ref].to(torch.int16) - outs[path].to(torch.int16)).abs()
+        res[f"diff_{path}_vs_{ref}"] = [int(d.max()), int((d > 0).sum())]
     print(json.dumps({"config": name, "frames": n, **res}), flush=True)
