@@ -36,6 +36,7 @@
 // virtual rows the edge rows' a, b (kept per thread in a small global scratch).
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "dhz_common.cuh"
 #include "dhz_internal.h"
@@ -76,9 +77,6 @@ struct FusedArgs {
 
 struct FusedShared {
   double f255[256];   // v / 255
-  double pt_ce[128];  // c_j^e, c_j = 1 + (j + 0.5)/128
-  double pt_ri[128];  // RN(1 / c_j)
-  double pt_p2[65];   // 2^(-k e)
   double2 thr2[256];  // (thr[k], thr[k+1]) output byte thresholds, thr[0] = -inf, thr[256] = +inf
   double sA[3];
   int mstar;
@@ -89,23 +87,56 @@ __device__ __forceinline__ double guide_n(uint32_t N) {
   return div_rb(u32_to_f64(N), k, rk);
 }
 
+// The general pow, kept out of line (rare paths; inlined it bloats the hot loops).
+__device__ __noinline__ double pow_general_ool(double x, double e) { return pow(x, e); }
+
+// Tables of pow_series (gray-world sums only).
+struct PowTables {
+  double ce[1024];  // c_j^e, c_j = 1 + (j + 0.5)/1024
+  double ri[1024];  // RN(1 / c_j)
+  double p2[65];    // 2^(-k e)
+};
+
+__device__ __forceinline__ void pow_tables_init(PowTables& T, double e) {
+  for (int j = threadIdx.x; j < 1024; j += blockDim.x) {
+    const double c = 1.0 + ((double)j + 0.5) / 1024.0;
+    T.ce[j] = pow(c, e);
+    T.ri[j] = __ddiv_rn(1.0, c);
+  }
+  for (int k = threadIdx.x; k <= 64; k += blockDim.x) T.p2[k] = exp2(-(double)k * e);
+}
+
 // x^e, x in [0, 1] (fixed e = inv_gamma): x = m 2^-k, m in [1, 2), c_j the centre of
-// m's 1/128 interval, m^e = c_j^e (1 + u)^e with |u| < 2^-8 and the binomial series
-// to degree 8.  Gray-world channel sums only (bytes never come from it).
-__device__ __forceinline__ double pow_series(double x, const FusedArgs& A, const FusedShared& S) {
+// m's 1/1024 interval, m^e = c_j^e (1 + u)^e with |u| < 2^-11 and the binomial series
+// to degree 4 (the u^5 term is below |C(e,5)| 2^-55: 3e-19 relative at e = 1/1.2,
+// 1e-13 at e = 16).  Gray-world channel sums only (bytes never come from it).
+__device__ __forceinline__ double pow_series(double x, const FusedArgs& A, const PowTables& S) {
   if (!(x > 0.0)) return 0.0;
   if (x >= 1.0) return 1.0;
   const long long bits = __double_as_longlong(x);
   const int k = 1023 - (int)(bits >> 52);  // x in [2^-k, 2^(1-k))
-  if (k > 64) return pow(x, A.inv_gamma);  // (never for recovered samples in practice)
-  const int j = (int)((bits >> 45) & 127);
+  if (k > 64) return pow_general_ool(x, A.inv_gamma);  // (never for recovered samples in practice)
+  const int j = (int)((bits >> 42) & 1023);
   const double m = __longlong_as_double((bits & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
-  const double u = __fma_rn(m, S.pt_ri[j], -1.0);
-  double s = A.h[8];
+  const double u = __fma_rn(m, S.ri[j], -1.0);
+  double s = A.h[4];
 #pragma unroll
-  for (int i = 7; i >= 1; --i) s = __fma_rn(s, u, A.h[i]);
+  for (int i = 3; i >= 1; --i) s = __fma_rn(s, u, A.h[i]);
   const double pm = __fma_rn(s, u, 1.0);  // (1 + u)^e
-  return __dmul_rn(__dmul_rn(S.pt_ce[j], pm), S.pt_p2[k]);
+  return __dmul_rn(__dmul_rn(S.ce[j], pm), S.p2[k]);
+}
+
+// One sample's gray-world term for the fixed-point channel sums: g = clip(x)^e with
+// x = RN(v/255 - A) rt + A (rt = RN(1/t~): one FMA, within 2 ulp of the exact
+// recovery, far below the 2^-38 resolution of the sums), returned as the bit pattern
+// of RN(g 2^38 + 1.5 2^52), whose low bits minus kGwBias are rint(g 2^38) (no
+// conversion instruction).
+constexpr unsigned long long kGwBias = 0x4338000000000000ull;
+__device__ __forceinline__ unsigned long long gw_term(double f255v, double Ac, double rt, const FusedArgs& A,
+                                                      const PowTables& PT) {
+  const double x = fmin(fmax(__fma_rn(__dsub_rn(f255v, Ac), rt, Ac), 0.0), 1.0);
+  const double g = A.gamma_is_one ? x : (A.pow_general ? pow_general_ool(x, A.inv_gamma) : pow_series(x, A, PT));
+  return (unsigned long long)__double_as_longlong(__fma_rn(g, 0x1p38, 0x1.8p52));
 }
 
 // Output byte of a recovered sample x: the k with thr[k] <= x < thr[k+1], walked from a
@@ -420,7 +451,8 @@ constexpr size_t kFusedSmem = (size_t)64 * kFMaxCols + 8 * 8 * kTw + 8ull * kPri
 // One segment: output rows [y0, y1) of strip `strip` of frame f.  R4 = r & 3 fixes the
 // alignment of the window reads.
 template <bool CLIP, int MODE, int R4>
-__device__ __noinline__ void fused_segment(const FusedArgs& A, FusedShared& S, unsigned char* dyn, int f, int strip,
+__device__ __noinline__ void fused_segment(const FusedArgs& A, FusedShared& S, const PowTables& PT, unsigned char* dyn,
+                                           int f, int strip,
                                            int y0, int y1, const FrameConst K, long long* __restrict__ edge,
                                            unsigned long long* __restrict__ bsum3) {
   using Q3T = typename Feat<CLIP>::Q3T;
@@ -668,18 +700,9 @@ __device__ __noinline__ void fused_segment(const FusedArgs& A, FusedShared& S, u
         ob[3 * c + 2] = quantize_pair(x2, S.thr2, guess_byte(x2, ig, 1.0f));
       } else {
         A.t_out[(int64_t)f * H * W + pix0 + c] = tt;
-        const double xv[3] = {x0, x1, x2};
-        unsigned long long q[3];
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const double xc = fmin(fmax(xv[ch], 0.0), 1.0);
-          const double gv =
-              A.gamma_is_one ? xc : (A.pow_general ? pow(xc, A.inv_gamma) : pow_series(xc, A, S));
-          q[ch] = __double2ull_rn(__dmul_rn(gv, 0x1p38));  // exact fixed-point sums
-        }
-        bs0 += q[0];
-        bs1 += q[1];
-        bs2 += q[2];
+        bs0 += gw_term(S.f255[R], A0, rt, A, PT) - kGwBias;
+        bs1 += gw_term(S.f255[G], A1, rt, A, PT) - kGwBias;
+        bs2 += gw_term(S.f255[B], A2, rt, A, PT) - kGwBias;
       }
     }
     if (MODE == 0) {
@@ -723,19 +746,13 @@ template <int MODE>
 __global__ void __maxnreg__(168) k_gf_fused(FusedArgs A, int nframes) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ FusedShared S;
+  __shared__ PowTables PT;
   const double e = A.inv_gamma;
   for (int v = threadIdx.x; v < 256; v += blockDim.x) {
     S.f255[v] = __ddiv_rn((double)v, 255.0);
     S.thr2[v] = make_double2(v == 0 ? -INFINITY : A.thr[v], v == 255 ? INFINITY : A.thr[v + 1]);
   }
-  if (MODE == 1 && !A.gamma_is_one) {
-    for (int j = threadIdx.x; j < 128; j += blockDim.x) {
-      const double c = 1.0 + ((double)j + 0.5) / 128.0;
-      S.pt_ce[j] = pow(c, e);
-      S.pt_ri[j] = __ddiv_rn(1.0, c);
-    }
-    for (int k = threadIdx.x; k <= 64; k += blockDim.x) S.pt_p2[k] = exp2(-(double)k * e);
-  }
+  if (MODE == 1 && !A.gamma_is_one) pow_tables_init(PT, e);
   const int64_t cols = (int64_t)nframes * A.nstrips;
   const int64_t total = cols * A.H;
   const int64_t b0 = total * blockIdx.x / gridDim.x, b1 = total * (blockIdx.x + 1) / gridDim.x;
@@ -768,8 +785,8 @@ __global__ void __maxnreg__(168) k_gf_fused(FusedArgs A, int nframes) {
     K.omt = __dsub_rn(1.0, A.t_min);
     const bool clip = S.mstar < 255;
 #define DHZ_SEG(R4)                                                                   \
-  if (clip) fused_segment<true, MODE, R4>(A, S, dyn, f, strip, yseg0, yseg1, K, edge, A.bsum + 3 * f); \
-  else fused_segment<false, MODE, R4>(A, S, dyn, f, strip, yseg0, yseg1, K, edge, A.bsum + 3 * f);
+  if (clip) fused_segment<true, MODE, R4>(A, S, PT, dyn, f, strip, yseg0, yseg1, K, edge, A.bsum + 3 * f); \
+  else fused_segment<false, MODE, R4>(A, S, PT, dyn, f, strip, yseg0, yseg1, K, edge, A.bsum + 3 * f);
     switch (A.r & 3) {
       case 0: DHZ_SEG(0) break;
       case 1: DHZ_SEG(1) break;
@@ -1122,44 +1139,64 @@ __device__ __forceinline__ void load_ab4(longlong2 (&v)[4], const longlong2* __r
 // window shrunk by kXMargin = 1e-6 on both sides (float edges rounded inwards), and
 // recomputed exactly (fp64, Markstein division, the exact thresholds) otherwise.
 constexpr double kXMargin = 1e-6;
+// Buckets of width 1/1024 over x in [0, 1) plus one for x >= 1.  Bucket j starts at byte
+// k0 = #{k >= 1 : thr[k] <= j/1024}; ent[j] = (lo(k0), hi(k0), lo(k0+1), hi(k0+1)), the
+// acceptance windows of k0 and k0 + 1 (threshold +- kXMargin, float edges rounded
+// inwards).  A sample is accepted when it lies in one of the two windows — one table
+// read, no walk — and takes the exact path otherwise (near a threshold, or a bucket
+// holding two thresholds, which gamma = 1.2 never has: its byte windows are wider
+// than 1/1024).
+constexpr int kXBuckets = 1024;
 struct XOutShared {
-  float2 win[256];      // (lo, hi) acceptance window of byte k
-  uint8_t guess[4104];  // byte of x = b / 4096, b <= 4096 (x >= 1) (the walk only goes up from it)
+  float4 ent[kXBuckets + 1];
+  uint8_t k0[kXBuckets + 8];
   float dq[3][256];     // RN_f(RN(v / 255) - A_c) of the segment's frame
   float af[3];
 };
 
 __device__ __forceinline__ void x_out_tables(XOutShared& X, const double* __restrict__ thr) {
-  for (int k = threadIdx.x; k < 256; k += blockDim.x) {
-    const float lo = k == 0 ? -INFINITY : __double2float_ru(__dadd_rn(thr[k], kXMargin));
-    const float hi = k == 255 ? INFINITY : __double2float_rd(__dsub_rn(thr[k + 1], kXMargin));
-    X.win[k] = make_float2(lo, hi);
-  }
-  for (int b = threadIdx.x; b <= 4096; b += blockDim.x) {
-    const double x = (double)b * (1.0 / 4096.0);
+  auto lo_of = [&](int k) -> float { return k <= 0 ? -INFINITY : (k > 255 ? INFINITY : __double2float_ru(__dadd_rn(thr[k], kXMargin))); };
+  auto hi_of = [&](int k) -> float { return k >= 255 ? INFINITY : __double2float_rd(__dsub_rn(thr[k + 1], kXMargin)); };
+  for (int j = threadIdx.x; j <= kXBuckets; j += blockDim.x) {
+    const double x = (double)j * (1.0 / kXBuckets);
     int lo = 0, hi = 255;  // largest k in [0, 255] with k == 0 or thr[k] <= x
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (thr[mid] <= x) lo = mid;
       else hi = mid - 1;
     }
-    X.guess[b] = (uint8_t)lo;
+    X.k0[j] = (uint8_t)lo;
+    X.ent[j] = make_float4(lo_of(lo), hi_of(lo), lo_of(lo + 1), hi_of(lo + 1));
   }
 }
 
 __device__ __forceinline__ uint32_t x_fast_byte(const XOutShared& X, float xf, bool& ok) {
-  const uint32_t b = min(__float2uint_rd(xf * 4096.0f), 4096u);  // (negative -> 0)
-  int k = X.guess[b];
-  float2 w = X.win[k];
-  while (xf >= w.y) w = X.win[++k];  // (win[255].y = +inf)
-  ok = ok && xf >= w.x;
-  return (uint32_t)k;
+  const uint32_t j = min(__float2uint_rd(xf * (float)kXBuckets), (uint32_t)kXBuckets);  // (negative -> 0)
+  const float4 e = X.ent[j];
+  const uint32_t k = X.k0[j];
+  const bool in0 = xf >= e.x && xf < e.y, in1 = xf >= e.z && xf < e.w;
+  ok = ok && (in0 || in1);
+  return k + (in1 ? 1u : 0u);
+}
+
+// Window sums of the thread's 4 consecutive strip columns from a per-warp exclusive
+// prefix E and the warp totals Tw: column c sums E[hi0 + c] - E[lo0 + c] + Tw[cor[c]],
+// cor[c] = the warp of its low end when the window crosses into the next warp, else
+// the zero slot kXTw - 1 (fixed for a segment: no per-row selects).
+template <typename U, int LOFF, int HOFF>
+__device__ __forceinline__ void xwin4(const U* __restrict__ E, const U* __restrict__ Tw, int lo0, int hi0,
+                                      const int (&cor)[4], U (&o)[4]) {
+  U hi[4], lo[4];
+  load4<U, LOFF>(E, lo0, lo);
+  load4<U, HOFF>(E, hi0, hi);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) o[c] = hi[c] - lo[c] + Tw[cor[c]];
 }
 
 // Pass 2 over output rows [y0, y1) of one strip: box of (a_q, b_q) -> t~ -> output.
 template <int MODE, int R4>
 __device__ __forceinline__ void x_out_segment(const FusedArgs& A, const FusedShared& S, const XOutShared& X,
-                                              unsigned char* dyn, int f, int strip, int y0, int y1,
+                                              const PowTables& PT, unsigned char* dyn, int f, int strip, int y0, int y1,
                                               unsigned long long* __restrict__ bsum3) {
   constexpr int LOFF = (4 - R4) & 3, HOFF = (R4 + 1) & 3;
   const int r = A.r, H = A.H, W = A.W;
@@ -1175,7 +1212,6 @@ __device__ __forceinline__ void x_out_segment(const FusedArgs& A, const FusedSha
 
   // per row parity b: [eA | eB | warp totals (2 words)], kXBuf2 bytes; then the staging
   constexpr int kXBuf2 = 2 * 8 * kXCols + 2 * 8 * kXTw;
-  unsigned char* d = dyn + 2 * kXBuf2;
   WinGeo g;
   {
     const int jo[4] = {4 * t, 4 * t + 1, 4 * t + 2, 4 * t + 3};
@@ -1184,6 +1220,14 @@ __device__ __forceinline__ void x_out_segment(const FusedArgs& A, const FusedSha
   const uint32_t outmask = G.outmask & g.valid;
   const bool vec_in = outmask == 15u && (W & 3) == 0 && ((uintptr_t)frame & 3) == 0;
   const bool vec_out = outmask == 15u && (W & 3) == 0 && ((uintptr_t)A.out & 3) == 0 && (A.out_fs & 3) == 0;
+  // output threads have all 4 windows inside the strip (the plan); cor[c] as above
+  const int lo0 = 4 * t - r, hi0 = 4 * t + r + 1;
+  int cor[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int lo = max(lo0 + c, 0), hi = min(hi0 + c, kXCols - 1);
+    cor[c] = (lo >> 7) != (hi >> 7) ? (lo >> 7) : kXTw - 1;
+  }
 #define CL(y) min(max((y), 0), H - 1)
   uint64_t SA[4] = {0, 0, 0, 0}, SB[4] = {0, 0, 0, 0};
   if (G.need) {
@@ -1208,18 +1252,26 @@ __device__ __forceinline__ void x_out_segment(const FusedArgs& A, const FusedSha
       }
     }
   }
-  // staging slots of this thread: [stage][row E/L][column] (16 B each), SoA over threads
-  // so a warp's 16-byte accesses are contiguous
-  longlong2* stg = reinterpret_cast<longlong2*>(d);
-  auto slot = [&](int row, int c) -> longlong2* { return stg + (row * 4 + c) * kXThreads + t; };
+  // staging slots of this thread: [row E/L][column] (16 B each), SoA over threads so a
+  // warp's 16-byte accesses are contiguous
+  longlong2* stg = reinterpret_cast<longlong2*>(dyn + 2 * kXBuf2) + t;
   auto stage_rows = [&](int YE, int YL) {
-    const longlong2* rE = abf + (int64_t)YE * W;
-    const longlong2* rL = abf + (int64_t)YL * W;
+    if (vec_ab) {
+      const longlong2* pE = abf + (int64_t)YE * W + G.xt;
+      const longlong2* pL = abf + (int64_t)YL * W + G.xt;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int x = vec_ab ? G.xt + c : jc[c];
-      cp_async16(slot(0, c), rE + x);
-      cp_async16(slot(1, c), rL + x);
+      for (int c = 0; c < 4; ++c) {
+        cp_async16(stg + c * kXThreads, pE + c);
+        cp_async16(stg + (4 + c) * kXThreads, pL + c);
+      }
+    } else {
+      const longlong2* pE = abf + (int64_t)YE * W;
+      const longlong2* pL = abf + (int64_t)YL * W;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        cp_async16(stg + c * kXThreads, pE + jc[c]);
+        cp_async16(stg + (4 + c) * kXThreads, pL + jc[c]);
+      }
     }
     cp_async_commit();
   };
@@ -1227,9 +1279,12 @@ __device__ __forceinline__ void x_out_segment(const FusedArgs& A, const FusedSha
   if (G.need && y0 + 1 < y1) stage_rows(CL(y0 + r + 1), CL(y0 - r));
   if (outmask) load_row(nC, frame, pitch, y0, G.xt, W, vec_in);
   const double A0 = S.sA[0], A1 = S.sA[1], A2 = S.sA[2];
+  const float tminf = (float)A.t_min;
   unsigned long long bs0 = 0, bs1 = 0, bs2 = 0;
-  for (int y = y0; y < y1; ++y) {
-    const int b = y & 1;
+  uint8_t* const obase = A.out + (int64_t)f * A.out_fs;
+
+  auto step = [&](auto Bc, int y) {
+    constexpr int b = decltype(Bc)::value;
     uint64_t* const eA = reinterpret_cast<uint64_t*>(dyn + b * kXBuf2);
     uint64_t* const eB = eA + kXCols;
     uint64_t* const tw = eB + kXCols;
@@ -1239,7 +1294,7 @@ __device__ __forceinline__ void x_out_segment(const FusedArgs& A, const FusedSha
       cp_async_wait_all();
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const longlong2 e = *slot(0, c), l = *slot(1, c);
+        const longlong2 e = stg[c * kXThreads], l = stg[(4 + c) * kXThreads];
         SA[c] += (uint64_t)e.x - (uint64_t)l.x;
         SB[c] += (uint64_t)e.y - (uint64_t)l.y;
       }
@@ -1247,61 +1302,73 @@ __device__ __forceinline__ void x_out_segment(const FusedArgs& A, const FusedSha
       if (outmask) load_row(nC, frame, pitch, y + 1, G.xt, W, vec_in);
     }
     __syncthreads();
-    if (!outmask) continue;
+    if (!outmask) return;
     uint64_t ba[4], bb[4];
-    window4<uint64_t, LOFF, HOFF>(eA, tw, g, 4 * t, 4 * t + 1, 4 * t + 2, 4 * t + 3, r, ba);
-    window4<uint64_t, LOFF, HOFF>(eB, tw + kXTw, g, 4 * t, 4 * t + 1, 4 * t + 2, 4 * t + 3, r, bb);
+    if (g.contig) {
+      xwin4<uint64_t, LOFF, HOFF>(eA, tw, lo0, hi0, cor, ba);
+      xwin4<uint64_t, LOFF, HOFF>(eB, tw + kXTw, lo0, hi0, cor, bb);
+    } else {
+      window4<uint64_t, LOFF, HOFF>(eA, tw, g, 4 * t, 4 * t + 1, 4 * t + 2, 4 * t + 3, r, ba);
+      window4<uint64_t, LOFF, HOFF>(eB, tw + kXTw, g, 4 * t, 4 * t + 1, 4 * t + 2, 4 * t + 3, r, bb);
+    }
     uint32_t ob[12];
+    double tv[4];
     const int64_t pix0 = (int64_t)y * W + G.xt;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       ob[3 * c] = ob[3 * c + 1] = ob[3 * c + 2] = 0;
+      tv[c] = 0.0;
       if (!(outmask >> c & 1)) continue;
       uint32_t R, Gc, B;
       rgb_of(wC, c, R, Gc, B);
-      const double mab = __dmul_rn(__ll2double_rn((long long)ba[c]), A.rqkk);
-      const double mbb = __dmul_rn(__ll2double_rn((long long)bb[c]), A.rqkk);
-      const double gg = guide_n(299u * R + 587u * Gc + 114u * B);
-      const double tt = fmin(fmax(__dadd_rn(__dmul_rn(mab, gg), mbb), A.t_min), 1.0);
+      const uint32_t N = 299u * R + 587u * Gc + 114u * B;
+      const double bad = __ll2double_rn((long long)ba[c]), bbd = __ll2double_rn((long long)bb[c]);
       if (MODE == 0) {
-        const float tf = __double2float_rn(tt);
+        // fast path: t~ to ~1e-15 (no exact roundings needed: every use below has a margin)
+        const double tr = __dmul_rn(__fma_rn(bad, __dmul_rn(u32_to_f64(N), 1.0 / 255000.0), bbd), A.rqkk);
+        const float tf = fminf(fmaxf(__double2float_rn(tr), tminf), 1.0f);
         float rtf;
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rtf) : "f"(tf));
         bool ok = true;
         uint32_t k0 = x_fast_byte(X, __fmaf_rn(X.dq[0][R], rtf, X.af[0]), ok);
         uint32_t k1 = x_fast_byte(X, __fmaf_rn(X.dq[1][Gc], rtf, X.af[1]), ok);
         uint32_t k2 = x_fast_byte(X, __fmaf_rn(X.dq[2][B], rtf, X.af[2]), ok);
-        if (!ok) {  // near a byte boundary: the exact fp64 recovery and thresholds
+        if (!ok) {  // near a byte boundary: t~ with the exact roundings, fp64 recovery, exact thresholds
+          const double tt = fmin(fmax(__dadd_rn(__dmul_rn(__dmul_rn(bad, A.rqkk), guide_n(N)), __dmul_rn(bbd, A.rqkk)),
+                                      A.t_min),
+                                 1.0);
           const double rt = __drcp_rn(tt);
-          const double x0 = recover_raw(S.f255[R], A0, tt, rt), x1 = recover_raw(S.f255[Gc], A1, tt, rt),
-                       x2 = recover_raw(S.f255[B], A2, tt, rt);
-          k0 = quantize_pair(x0, S.thr2, (int)k0);
-          k1 = quantize_pair(x1, S.thr2, (int)k1);
-          k2 = quantize_pair(x2, S.thr2, (int)k2);
+          k0 = quantize_pair(recover_raw(S.f255[R], A0, tt, rt), S.thr2, (int)k0);
+          k1 = quantize_pair(recover_raw(S.f255[Gc], A1, tt, rt), S.thr2, (int)k1);
+          k2 = quantize_pair(recover_raw(S.f255[B], A2, tt, rt), S.thr2, (int)k2);
         }
         ob[3 * c] = k0;
         ob[3 * c + 1] = k1;
         ob[3 * c + 2] = k2;
       } else {
-        A.t_out[(int64_t)f * H * W + pix0 + c] = tt;
+        const double tt =
+            fmin(fmax(__dadd_rn(__dmul_rn(__dmul_rn(bad, A.rqkk), guide_n(N)), __dmul_rn(bbd, A.rqkk)), A.t_min), 1.0);
+        tv[c] = tt;
         const double rt = __drcp_rn(tt);
-        const double xv[3] = {recover_raw(S.f255[R], A0, tt, rt), recover_raw(S.f255[Gc], A1, tt, rt),
-                              recover_raw(S.f255[B], A2, tt, rt)};
-        unsigned long long q[3];
+        bs0 += gw_term(S.f255[R], A0, rt, A, PT) - kGwBias;
+        bs1 += gw_term(S.f255[Gc], A1, rt, A, PT) - kGwBias;
+        bs2 += gw_term(S.f255[B], A2, rt, A, PT) - kGwBias;
+      }
+    }
+    if (MODE == 1) {  // t~ for the apply pass, 32 bytes per thread
+      const int64_t ti = (int64_t)f * H * W + pix0;
+      double* trow = A.t_out + ti;
+      if (outmask == 15u && (ti & 1) == 0) {
+        reinterpret_cast<double2*>(trow)[0] = make_double2(tv[0], tv[1]);
+        reinterpret_cast<double2*>(trow)[1] = make_double2(tv[2], tv[3]);
+      } else {
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const double xc = fmin(fmax(xv[ch], 0.0), 1.0);
-          const double gv =
-              A.gamma_is_one ? xc : (A.pow_general ? pow(xc, A.inv_gamma) : pow_series(xc, A, S));
-          q[ch] = __double2ull_rn(__dmul_rn(gv, 0x1p38));  // exact fixed-point sums
-        }
-        bs0 += q[0];
-        bs1 += q[1];
-        bs2 += q[2];
+        for (int c = 0; c < 4; ++c)
+          if (outmask >> c & 1) trow[c] = tv[c];
       }
     }
     if (MODE == 0) {
-      uint8_t* orow = A.out + (int64_t)f * A.out_fs + pix0 * 3;
+      uint8_t* orow = obase + pix0 * 3;
       if (vec_out) {
         uint32_t* o32 = reinterpret_cast<uint32_t*>(orow);
         o32[0] = ob[0] | (ob[1] << 8) | (ob[2] << 16) | (ob[3] << 24);
@@ -1317,7 +1384,13 @@ __device__ __forceinline__ void x_out_segment(const FusedArgs& A, const FusedSha
           }
       }
     }
+  };
+  int y = y0;
+  for (; y + 1 < y1; y += 2) {  // two rows per trip: the prefix buffers at fixed offsets
+    step(std::integral_constant<int, 0>{}, y);
+    step(std::integral_constant<int, 1>{}, y + 1);
   }
+  if (y < y1) step(std::integral_constant<int, 0>{}, y);
 #undef CL
   if (MODE == 1) {  // per-frame channel sums (integer: order-free)
     unsigned long long v[3] = {bs0, bs1, bs2};
@@ -1335,20 +1408,19 @@ __global__ void __launch_bounds__(kXThreads, 2) k_gx_out(FusedArgs A, int nframe
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ FusedShared S;
   __shared__ XOutShared X;
+  __shared__ PowTables PT;
   if (MODE == 0) x_out_tables(X, A.thr);
+  if (threadIdx.x < 4) {  // the zero slots of the warp totals (both words, both row parities)
+    constexpr int kXBuf2 = 2 * 8 * kXCols + 2 * 8 * kXTw;
+    uint64_t* tw = reinterpret_cast<uint64_t*>(dyn + (threadIdx.x >> 1) * kXBuf2) + 2 * kXCols;
+    tw[(threadIdx.x & 1) * kXTw + kXTw - 1] = 0;
+  }
   const double e = A.inv_gamma;
   for (int v = threadIdx.x; v < 256; v += blockDim.x) {
     S.f255[v] = __ddiv_rn((double)v, 255.0);
     S.thr2[v] = make_double2(v == 0 ? -INFINITY : A.thr[v], v == 255 ? INFINITY : A.thr[v + 1]);
   }
-  if (MODE == 1 && !A.gamma_is_one) {
-    for (int j = threadIdx.x; j < 128; j += blockDim.x) {
-      const double c = 1.0 + ((double)j + 0.5) / 128.0;
-      S.pt_ce[j] = pow(c, e);
-      S.pt_ri[j] = __ddiv_rn(1.0, c);
-    }
-    for (int k = threadIdx.x; k <= 64; k += blockDim.x) S.pt_p2[k] = exp2(-(double)k * e);
-  }
+  if (MODE == 1 && !A.gamma_is_one) pow_tables_init(PT, e);
   const int64_t cols = (int64_t)nframes * A.nstrips;
   const int64_t total = cols * A.H;
   const int64_t b0 = total * blockIdx.x / gridDim.x, b1 = total * (blockIdx.x + 1) / gridDim.x;
@@ -1371,10 +1443,10 @@ __global__ void __launch_bounds__(kXThreads, 2) k_gx_out(FusedArgs A, int nframe
     }
     __syncthreads();
     switch (A.r & 3) {
-      case 0: x_out_segment<MODE, 0>(A, S, X, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
-      case 1: x_out_segment<MODE, 1>(A, S, X, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
-      case 2: x_out_segment<MODE, 2>(A, S, X, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
-      default: x_out_segment<MODE, 3>(A, S, X, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
+      case 0: x_out_segment<MODE, 0>(A, S, X, PT, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
+      case 1: x_out_segment<MODE, 1>(A, S, X, PT, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
+      case 2: x_out_segment<MODE, 2>(A, S, X, PT, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
+      default: x_out_segment<MODE, 3>(A, S, X, PT, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
     }
   }
 }

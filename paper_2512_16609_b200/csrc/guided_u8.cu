@@ -420,50 +420,146 @@ k_gf_thresholds(const double* __restrict__ part, int nparts, int64_t npx, double
   out[k] = __longlong_as_double(hi);
 }
 
-// gray-world apply: out = #thresholds <= recovered x (per channel).  Four
-// independent pixels per thread and iteration keep enough loads in flight.
-__global__ void __launch_bounds__(256)
-k_gf_apply(const uint8_t* __restrict__ in, int64_t in_fs, int64_t npx, const double* __restrict__ t_in,
-           const double* __restrict__ airlight, const double* __restrict__ thr, const float* __restrict__ gains,
-           double inv_gamma, uint8_t* __restrict__ out, int64_t out_fs) {
-  constexpr int U = 4;
-  __shared__ double s_f[256], s_thr[3][256];
-  const int f = blockIdx.y;
-  s_f[threadIdx.x] = u8f(threadIdx.x);
-  for (int c = 0; c < 3; ++c) s_thr[c][threadIdx.x] = thr[((int64_t)f * 3 + c) * 256 + threadIdx.x];
+// gray-world apply, fp32 fast path: the byte of channel c is the number of the
+// frame's balanced thresholds thr_c[k] <= x (exact, k_gf_thresholds).  As in the
+// two-pass output (guided_fused.cu), x is first formed in fp32 (|xf - x| < 4.6e-7
+// wherever a window edge is finite) and accepted when it lies inside a byte window
+// shrunk by 1e-6 (one bucket table read per sample); otherwise the exact fp64
+// recovery and threshold walk decide.  Persistent CTAs over the batch's 4-pixel
+// groups; the per-frame tables are rebuilt when a CTA's range enters a new frame.
+constexpr int kApBuckets = 1024;
+constexpr double kApMargin = 1e-6;
+struct ApplyShared {
+  float4 ent[3][kApBuckets + 1];
+  uint8_t k0[3][kApBuckets + 8];
+  float dq[3][256];
+  double f255[256];
+  double thr[3][256];
+  float af[3];
+};
+
+__device__ void apply_tables(ApplyShared& S, const double* __restrict__ thr, const double* __restrict__ airlight,
+                             int f) {
+  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) {
+    const int c = i >> 8, v = i & 255;
+    S.thr[c][v] = thr[((int64_t)f * 3 + c) * 256 + v];
+    S.dq[c][v] = __double2float_rn(__dsub_rn(S.f255[v], airlight[3 * f + c]));
+    if (v == 0) S.af[c] = __double2float_rn(airlight[3 * f + c]);
+  }
   __syncthreads();
-  const double A0 = airlight[3 * f], A1 = airlight[3 * f + 1], A2 = airlight[3 * f + 2];
-  const float gn0 = gains[3 * f], gn1 = gains[3 * f + 1], gn2 = gains[3 * f + 2];
-  const float ig = (float)inv_gamma;
-  const uint8_t* fi = in + (int64_t)f * in_fs;
-  uint8_t* fo = out + (int64_t)f * out_fs;
-  const double* ft = t_in + (int64_t)f * npx;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < npx; p0 += U * stride) {
-    double t[U];
-    uint32_t v[U][3];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t p = min(p0 + u * stride, npx - 1);
-      t[u] = ft[p];
-      v[u][0] = fi[3 * p];
-      v[u][1] = fi[3 * p + 1];
-      v[u][2] = fi[3 * p + 2];
+  for (int i = threadIdx.x; i < 3 * (kApBuckets + 1); i += blockDim.x) {
+    const int c = i / (kApBuckets + 1), j = i - c * (kApBuckets + 1);
+    const double* T = S.thr[c];
+    const double x = (double)j * (1.0 / kApBuckets);
+    int lo = 0, hi = 255;  // largest k in [0, 255] with k == 0 or T[k] <= x
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (T[mid] <= x) lo = mid;
+      else hi = mid - 1;
     }
+    auto lo_of = [&](int k) -> float {
+      return k <= 0 ? -INFINITY : (k > 255 ? INFINITY : __double2float_ru(__dadd_rn(T[k], kApMargin)));
+    };
+    auto hi_of = [&](int k) -> float { return k >= 255 ? INFINITY : __double2float_rd(__dsub_rn(T[k + 1], kApMargin)); };
+    S.k0[c][j] = (uint8_t)lo;
+    S.ent[c][j] = make_float4(lo_of(lo), hi_of(lo), lo_of(lo + 1), hi_of(lo + 1));
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t apply_byte(const ApplyShared& S, int c, float xf, bool& ok) {
+  const uint32_t j = min(__float2uint_rd(xf * (float)kApBuckets), (uint32_t)kApBuckets);
+  const float4 e = S.ent[c][j];
+  const uint32_t k = S.k0[c][j];
+  const bool in0 = xf >= e.x && xf < e.y, in1 = xf >= e.z && xf < e.w;
+  ok = ok && (in0 || in1);
+  return k + (in1 ? 1u : 0u);
+}
+
+__global__ void __launch_bounds__(256, 3)
+k_gf_apply2(const uint8_t* __restrict__ in, int64_t in_fs, int n, int64_t npx, const double* __restrict__ t_in,
+            const double* __restrict__ airlight, const double* __restrict__ thr, uint8_t* __restrict__ out,
+            int64_t out_fs) {
+  extern __shared__ __align__(16) unsigned char apply_smem[];
+  ApplyShared& S = *reinterpret_cast<ApplyShared*>(apply_smem);
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) S.f255[v] = u8f(v);
+  const int64_t G = (npx + 3) >> 2;  // 4-pixel groups per frame
+  const int64_t total = (int64_t)n * G;
+  const int64_t g0 = total * blockIdx.x / gridDim.x, g1 = total * (blockIdx.x + 1) / gridDim.x;
+  const bool vec = (npx & 3) == 0 && (in_fs & 3) == 0 && (out_fs & 3) == 0 && ((uintptr_t)in & 3) == 0 &&
+                   ((uintptr_t)out & 3) == 0 && ((uintptr_t)t_in & 15) == 0;
+  for (int64_t s0 = g0; s0 < g1;) {
+    const int f = (int)(s0 / G);
+    const int64_t s1 = min(g1, (int64_t)(f + 1) * G);
+    __syncthreads();  // the previous frame's readers are done
+    apply_tables(S, thr, airlight, f);
+    const double A0 = airlight[3 * f], A1 = airlight[3 * f + 1], A2 = airlight[3 * f + 2];
+    const uint8_t* fi = in + (int64_t)f * in_fs;
+    uint8_t* fo = out + (int64_t)f * out_fs;
+    const double* ft = t_in + (int64_t)f * npx;
+    for (int64_t g = s0 + threadIdx.x; g < s1; g += blockDim.x) {
+      const int64_t p0 = (g - (int64_t)f * G) * 4;
+      const int np = (int)min((int64_t)4, npx - p0);
+      double t[4];
+      uint32_t w[3];
+      if (vec) {
+        const double2 ta = *reinterpret_cast<const double2*>(ft + p0);
+        const double2 tb = *reinterpret_cast<const double2*>(ft + p0 + 2);
+        t[0] = ta.x; t[1] = ta.y; t[2] = tb.x; t[3] = tb.y;
+        const uint32_t* q = reinterpret_cast<const uint32_t*>(fi + 3 * p0);
+        w[0] = __ldg(q); w[1] = __ldg(q + 1); w[2] = __ldg(q + 2);
+      } else {
+        uint32_t b[12];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t p = p0 + u * stride;
-      if (p < npx) {
-        const double rt = __drcp_rn(t[u]);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double Ac = c == 0 ? A0 : (c == 1 ? A1 : A2);
-          const float gc = c == 0 ? gn0 : (c == 1 ? gn1 : gn2);
-          const double x = recover_raw(s_f[v[u][c]], Ac, t[u], rt);
-          fo[3 * p + c] = (uint8_t)quantize_thr_from(x, s_thr[c], guess_byte(x, ig, gc));
+        for (int u = 0; u < 4; ++u) {
+          const int64_t p = p0 + min(u, np - 1);
+          t[u] = ft[p];
+          b[3 * u] = fi[3 * p];
+          b[3 * u + 1] = fi[3 * p + 1];
+          b[3 * u + 2] = fi[3 * p + 2];
         }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) w[q] = b[4 * q] | (b[4 * q + 1] << 8) | (b[4 * q + 2] << 16) | (b[4 * q + 3] << 24);
+      }
+      uint32_t ob[12];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t v0 = (w[(3 * u) >> 2] >> (8 * ((3 * u) & 3))) & 255u;
+        const uint32_t v1 = (w[(3 * u + 1) >> 2] >> (8 * ((3 * u + 1) & 3))) & 255u;
+        const uint32_t v2 = (w[(3 * u + 2) >> 2] >> (8 * ((3 * u + 2) & 3))) & 255u;
+        float rtf;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rtf) : "f"(__double2float_rn(t[u])));
+        bool ok = true;
+        uint32_t k0 = apply_byte(S, 0, __fmaf_rn(S.dq[0][v0], rtf, S.af[0]), ok);
+        uint32_t k1 = apply_byte(S, 1, __fmaf_rn(S.dq[1][v1], rtf, S.af[1]), ok);
+        uint32_t k2 = apply_byte(S, 2, __fmaf_rn(S.dq[2][v2], rtf, S.af[2]), ok);
+        if (!ok) {
+          const double rt = __drcp_rn(t[u]);
+          k0 = quantize_thr_from(recover_raw(S.f255[v0], A0, t[u], rt), S.thr[0], (int)min(k0, 255u));
+          k1 = quantize_thr_from(recover_raw(S.f255[v1], A1, t[u], rt), S.thr[1], (int)min(k1, 255u));
+          k2 = quantize_thr_from(recover_raw(S.f255[v2], A2, t[u], rt), S.thr[2], (int)min(k2, 255u));
+        }
+        ob[3 * u] = k0;
+        ob[3 * u + 1] = k1;
+        ob[3 * u + 2] = k2;
+      }
+      uint8_t* o = fo + 3 * p0;
+      if (vec) {
+        uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
+        o32[0] = ob[0] | (ob[1] << 8) | (ob[2] << 16) | (ob[3] << 24);
+        o32[1] = ob[4] | (ob[5] << 8) | (ob[6] << 16) | (ob[7] << 24);
+        o32[2] = ob[8] | (ob[9] << 8) | (ob[10] << 16) | (ob[11] << 24);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < np) {
+            o[3 * u] = (uint8_t)ob[3 * u];
+            o[3 * u + 1] = (uint8_t)ob[3 * u + 1];
+            o[3 * u + 2] = (uint8_t)ob[3 * u + 2];
+          }
       }
     }
+    s0 = s1;
   }
 }
 
@@ -504,8 +600,16 @@ int guided_seg_rows(int H, int W, int r, int cpt) {
 cudaError_t guided_apply(const uint8_t* in, int64_t in_fs, int n, int64_t npx, const double* t,
                          const double* airlight, const double* thr, const float* gains, double gamma, uint8_t* out,
                          int64_t out_fs, cudaStream_t st) {
-  dim3 g2((unsigned)std::max<int64_t>(1, std::min<int64_t>(2048, (npx + 1023) / 1024)), n);
-  k_gf_apply<<<g2, 256, 0, st>>>(in, in_fs, npx, t, airlight, thr, gains, 1.0 / gamma, out, out_fs);
+  (void)gains;
+  (void)gamma;
+  const int smem = (int)sizeof(ApplyShared);
+  cudaError_t e = cudaFuncSetAttribute(k_gf_apply2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t groups = (int64_t)n * ((npx + 3) / 4);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(3LL * sms, (groups + 255) / 256));
+  k_gf_apply2<<<grid, 256, smem, st>>>(in, in_fs, n, npx, t, airlight, thr, out, out_fs);
   return cudaGetLastError();
 }
 
@@ -607,8 +711,7 @@ cudaError_t guided_recover_u8(const uint8_t* in, int64_t in_fs, int n, int H, in
       double* bthr = part + 3LL * nparts * c;
       float* gains = reinterpret_cast<float*>(bthr + 3LL * 256 * c);
       balance_thresholds(part, nparts, c, npx, gamma, bthr, gains, st);
-      dim3 g2((unsigned)std::max<int64_t>(1, std::min<int64_t>(2048, (npx + 1023) / 1024)), c);
-      k_gf_apply<<<g2, 256, 0, st>>>(fin, in_fs, npx, t, fA, bthr, gains, inv_g, fout, out_fs);
+      if ((ae = guided_apply(fin, in_fs, c, npx, t, fA, bthr, gains, gamma, fout, out_fs, st)) != cudaSuccess) return ae;
     }
   }
   return cudaGetLastError();

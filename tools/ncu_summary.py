@@ -35,5 +35,5 @@ for r in rows[2:]:
             i = hdr.index(k)
             print(f"   {label:22s} {r[i]:>18s} {units[i]}")
     st = sorted(((float(r[hdr.index(h)] or 0), h.replace("smsp__pcsamp_warps_issue_stalled_", "")) for h in stalls),
-                reverse=True)[:6]
+                reverse=True)[:int(__import__("os").environ.get("NSTALL", "6"))]
     print("   top stalls:", ", ".join(f"{n}={int(v)}" for v, n in st))
