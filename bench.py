@@ -64,21 +64,25 @@ def _base(cfg):
     return cfg[:2]
 # algorithmic HBM bytes per pixel: dark 4 + select 1 + recover 6 (+3 balance);
 # image mode + balance 29 (dark 4 + select 1 + guided 7 (read I 3, write t~ fp32 4) + recover 6
-# + t~ read 4 + balance 3 + 4).  The strip kernels' own design moves more (pass 1 writes a, b
-# 16 B/px, pass 2 reads them, t~ is fp64): DESIGN_BYTES, reported beside it.
+# + t~ read 4 + balance 3 + 4).  The exact two-pass guided filter's own design moves more
+# (pass 1 writes the fixed-point a, b 16 B/px, pass 2 reads them for the entering and the
+# leaving row 32, t~ is fp64 8 written + 8 read, apply reads I again 3): DESIGN_BYTES,
+# reported beside it (4 + 1 + (3 + 16) + (32 + 3 + 8) + (8 + 3 + 3) = 81 B/px).
 ALG_BYTES = {"c1": 11, "c3": 11, "c4": 14, "c2": 29, "c5": 29,
              # resize path per INPUT pixel (1080p -> 640x480, 0.148 output px per input px): dark pass
              # reads I 3 + writes dark 8*0.148, select reads dark 8*0.148, recover reads I 3 + writes 3*0.148
              "c3d": round(6 + 19 * (640 * 480) / (1920 * 1080), 2)}
-DESIGN_BYTES = {"c2": 62, "c5": 62}
+DESIGN_BYTES = {"c2": 81, "c5": 81}
 # the guided stage (guided filter + recovery [+ balance]) at §8(d) bytes: 29 - dark 4 - select 1
 GUIDED_BYTES = {False: 13, True: 24}
 
 
 def _guided_chunk(n, H, W, params):
-    """Frames per guided-filter chunk (csrc/guided_u8.cu guided_chunk)."""
+    """Frames per guided-filter chunk (csrc/guided_fused.cu x_chunk, the default two-pass form)."""
     per = (24.0 if params.balance_enabled() else 16.0) * H * W
-    return int(max(1.0, min(float(n), 4.0e9 / per)))
+    cap = int(max(1.0, min(float(n), 12.0e9 / per)))
+    chunks = (n + cap - 1) // cap
+    return (n + chunks - 1) // chunks
 
 
 def _ncu_traffic_per_px():
@@ -444,13 +448,13 @@ def main():
     elif native:
         gb = GUIDED_BYTES[params.balance_enabled()] * n * npx
         g_gbs = gb / (stage_ms[2] / 1000.0) / 1e9
-        roof = {"bound": "hbm", "kernel": "guided stage at SURVEY §8(d) bytes (%d B/px): k_gf_pass1 + k_gf_pass2 "
-                "(+ k_gf_thresholds + k_gf_apply)" % GUIDED_BYTES[params.balance_enabled()],
+        roof = {"bound": "hbm", "kernel": "guided stage at SURVEY §8(d) bytes (%d B/px): k_gx_ab + k_gx_out "
+                "(+ k_gf_thresholds + k_gf_apply2)" % GUIDED_BYTES[params.balance_enabled()],
                 "achieved": round(g_gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(g_gbs / peak, 4),
                 "traffic": None, "peak_kind": peak_kind, "alg_bytes_per_launch": gb,
                 "launch_ms": round(stage_ms[2], 4)}
-        # K1 + the 6 select kernels + pass1 + pass2 (+ thresholds + apply) per <=4 GB chunk of frames
-        launches = 7 + (4 if params.balance_enabled() else 2) * math.ceil(n / _guided_chunk(n, H, W, params))
+        # K1 + the 6 select kernels + pass1 + pass2 (+ sums, thresholds, apply) per <=12 GB chunk of frames
+        launches = 7 + (5 if params.balance_enabled() else 2) * math.ceil(n / _guided_chunk(n, H, W, params))
     else:
         roof = {"bound": "hbm", "kernel": "float64 image-mode pipeline (whole step)", "achieved": round(pipe_gbs, 1),
                 "peak": peak, "unit": "GB/s", "frac": round(pipe_gbs / peak, 4), "traffic": None,

@@ -1461,8 +1461,9 @@ XPlan x_plan(int n, int H, int W, int r, int sms) {
   P.nstrips = (W + ow_max - 1) / ow_max;
   P.ow = (((W + P.nstrips - 1) / P.nstrips) + 3) & ~3;
   const int64_t rows = (int64_t)n * P.nstrips * H;
-  // a segment pays a (2r+1)-row warm-up: keep >= 2r+1 (and >= 16) output rows per CTA
-  const int64_t by_rows = std::max<int64_t>(1, rows / std::max(16, 2 * r + 1));
+  // a segment pays a (2r+1)-row warm-up (loads + adds only, ~1/4 of a row step): small
+  // batches still take every SM, down to 8 output rows per CTA
+  const int64_t by_rows = std::max<int64_t>(1, rows / 8);
   P.ctas = (int)std::min<int64_t>(2LL * sms, by_rows);
   return P;
 }

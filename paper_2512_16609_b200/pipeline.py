@@ -449,7 +449,9 @@ def dehaze_host_batch(frames, params=None, out=None, airlight=None, chunk=None, 
     if n == 0:
         return out, airlight
     if chunk is None:
-        chunk = max(1, min(n, (48 << 20) // (3 * H * W)))
+        # ~96 MiB of input per ring step (tools/host_chunk_probe.py: C4 2-4 frames 63 ms vs
+        # 66.7 ms one frame per step; C3 16 frames 39.9 vs 40.4 ms for 7)
+        chunk = max(1, min(n, (96 << 20) // (3 * H * W)))
     import threading
 
     # per (device, thread), like engine_for: concurrent callers never share staging buffers;
