@@ -243,6 +243,66 @@ __device__ __forceinline__ double pow_tab(double x, double e, const PowTables& T
 // ((x - A) / t) + A without the final clip: where the value only feeds the byte
 // thresholds (x < 0 -> byte 0, x > 1 -> the byte of 1) or pow_tab (0 / 1 outside
 // (0, 1)), clipping first gives the same result, so the clip is skipped there.
+// ---- fp32 fast path of an output byte ----------------------------------------------
+// The exact byte of a recovered sample x is #{k >= 1 : thr[k] <= x} (thr[1..255], from
+// the host's np.power, quant.py, or per frame with gray-world gains).  A caller forms xf,
+// the same x in fp32 (|xf - x| < 4.6e-7 wherever |x - A| <= 1, i.e. wherever a window's
+// finite edge lies: one FMA of a float copy of t~'s approximate reciprocal (rel. error
+// < 2^-22) and RN_f(RN(v - A)) (rel. 2^-24)), and looks it up in a bucket table:
+// buckets of width 1/1024 over [0, 1) plus one for x >= 1; bucket j starts at byte
+// k0 = #{k : thr[k] <= j/1024} and holds the acceptance windows of k0 and k0 + 1
+// (threshold +- kByteMargin, float edges rounded inwards).  A sample outside both
+// windows (near a threshold, or in a bucket holding two thresholds — gamma = 1.2 has
+// none: its byte windows are wider than 1/1024) goes to the caller's exact fp64 path.
+constexpr int kByteBuckets = 1024;
+constexpr double kByteMargin = 1e-6;
+struct ByteBuckets {
+  float4 ent[kByteBuckets + 1];  // (lo(k0), hi(k0), lo(k0 + 1), hi(k0 + 1))
+  uint8_t k0[kByteBuckets + 8];
+};
+
+// Block-cooperative build from thr[0..255] (thr[0] unused; +inf = unreachable level);
+// the caller synchronises before use.
+__device__ __forceinline__ void byte_buckets_build(ByteBuckets& B, const double* __restrict__ thr) {
+  auto lo_of = [&](int k) -> float {
+    return k <= 0 ? -INFINITY : (k > 255 ? INFINITY : __double2float_ru(__dadd_rn(thr[k], kByteMargin)));
+  };
+  auto hi_of = [&](int k) -> float { return k >= 255 ? INFINITY : __double2float_rd(__dsub_rn(thr[k + 1], kByteMargin)); };
+  for (int j = threadIdx.x; j <= kByteBuckets; j += blockDim.x) {
+    const double x = (double)j * (1.0 / kByteBuckets);
+    int lo = 0, hi = 255;  // largest k in [0, 255] with k == 0 or thr[k] <= x
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (thr[mid] <= x) lo = mid;
+      else hi = mid - 1;
+    }
+    B.k0[j] = (uint8_t)lo;
+    B.ent[j] = make_float4(lo_of(lo), hi_of(lo), lo_of(lo + 1), hi_of(lo + 1));
+  }
+}
+
+// Byte of xf from the table; ok stays true only if xf lies inside an acceptance window.
+__device__ __forceinline__ uint32_t byte_bucket(const ByteBuckets& B, float xf, bool& ok) {
+  const uint32_t j = min(__float2uint_rd(xf * (float)kByteBuckets), (uint32_t)kByteBuckets);  // (negative -> 0)
+  const float4 e = B.ent[j];
+  const uint32_t k = B.k0[j];
+  const bool in0 = xf >= e.x && xf < e.y, in1 = xf >= e.z && xf < e.w;
+  ok = ok && (in0 || in1);
+  return k + (in1 ? 1u : 0u);
+}
+
+// 1 / t in fp32 (rcp.approx: rel. error < 2^-22), for the fast path above.
+__device__ __forceinline__ float rcp_approx(float t) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(t));
+  return r;
+}
+
+// min / max of two non-NaN doubles as one compare and two selects (fmin / fmax add a
+// NaN fix-up; every operand here is finite, and no -0.0 meets a +0.0 where it matters).
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double dmax(double a, double b) { return b > a ? b : a; }
+
 __device__ __forceinline__ double recover_raw(double x, double A, double t, double rt) {
   return __dadd_rn(div_rb(__dsub_rn(x, A), t, rt), A);
 }

@@ -1130,54 +1130,13 @@ __device__ __forceinline__ void load_ab4(longlong2 (&v)[4], const longlong2* __r
   }
 }
 
-// fp32 fast path of the output bytes (pass 2 without balance).  The exact byte of a
-// recovered sample x (fp64, from t~) is the k with thr[k] <= x < thr[k+1].  xf, the
-// same x in fp32 from a float copy of t~ (RN), its approximate reciprocal (rcp.approx,
-// rel. error < 2^-22) and dq = RN_f(RN(v/255) - A) (rel. 2^-24) with one FFMA,
-// satisfies |xf - x| <= |x - A| 2^-21.4 + 2^-24 < 4.6e-7 wherever |x - A| <= 1, i.e.
-// wherever a byte window's finite edge lies; the byte is accepted when xf lies in its
-// window shrunk by kXMargin = 1e-6 on both sides (float edges rounded inwards), and
-// recomputed exactly (fp64, Markstein division, the exact thresholds) otherwise.
-constexpr double kXMargin = 1e-6;
-// Buckets of width 1/1024 over x in [0, 1) plus one for x >= 1.  Bucket j starts at byte
-// k0 = #{k >= 1 : thr[k] <= j/1024}; ent[j] = (lo(k0), hi(k0), lo(k0+1), hi(k0+1)), the
-// acceptance windows of k0 and k0 + 1 (threshold +- kXMargin, float edges rounded
-// inwards).  A sample is accepted when it lies in one of the two windows — one table
-// read, no walk — and takes the exact path otherwise (near a threshold, or a bucket
-// holding two thresholds, which gamma = 1.2 never has: its byte windows are wider
-// than 1/1024).
-constexpr int kXBuckets = 1024;
+// fp32 fast path of the output bytes (pass 2 without balance): byte_bucket
+// (dhz_common.cuh) on xf = RN_f(RN(v/255) - A) * rcp(t~) + A, the exact path otherwise.
 struct XOutShared {
-  float4 ent[kXBuckets + 1];
-  uint8_t k0[kXBuckets + 8];
+  ByteBuckets bk;
   float dq[3][256];     // RN_f(RN(v / 255) - A_c) of the segment's frame
   float af[3];
 };
-
-__device__ __forceinline__ void x_out_tables(XOutShared& X, const double* __restrict__ thr) {
-  auto lo_of = [&](int k) -> float { return k <= 0 ? -INFINITY : (k > 255 ? INFINITY : __double2float_ru(__dadd_rn(thr[k], kXMargin))); };
-  auto hi_of = [&](int k) -> float { return k >= 255 ? INFINITY : __double2float_rd(__dsub_rn(thr[k + 1], kXMargin)); };
-  for (int j = threadIdx.x; j <= kXBuckets; j += blockDim.x) {
-    const double x = (double)j * (1.0 / kXBuckets);
-    int lo = 0, hi = 255;  // largest k in [0, 255] with k == 0 or thr[k] <= x
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (thr[mid] <= x) lo = mid;
-      else hi = mid - 1;
-    }
-    X.k0[j] = (uint8_t)lo;
-    X.ent[j] = make_float4(lo_of(lo), hi_of(lo), lo_of(lo + 1), hi_of(lo + 1));
-  }
-}
-
-__device__ __forceinline__ uint32_t x_fast_byte(const XOutShared& X, float xf, bool& ok) {
-  const uint32_t j = min(__float2uint_rd(xf * (float)kXBuckets), (uint32_t)kXBuckets);  // (negative -> 0)
-  const float4 e = X.ent[j];
-  const uint32_t k = X.k0[j];
-  const bool in0 = xf >= e.x && xf < e.y, in1 = xf >= e.z && xf < e.w;
-  ok = ok && (in0 || in1);
-  return k + (in1 ? 1u : 0u);
-}
 
 // Window sums of the thread's 4 consecutive strip columns from a per-warp exclusive
 // prefix E and the warp totals Tw: column c sums E[hi0 + c] - E[lo0 + c] + Tw[cor[c]],
@@ -1330,9 +1289,9 @@ __device__ __forceinline__ void x_out_segment(const FusedArgs& A, const FusedSha
         float rtf;
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rtf) : "f"(tf));
         bool ok = true;
-        uint32_t k0 = x_fast_byte(X, __fmaf_rn(X.dq[0][R], rtf, X.af[0]), ok);
-        uint32_t k1 = x_fast_byte(X, __fmaf_rn(X.dq[1][Gc], rtf, X.af[1]), ok);
-        uint32_t k2 = x_fast_byte(X, __fmaf_rn(X.dq[2][B], rtf, X.af[2]), ok);
+        uint32_t k0 = byte_bucket(X.bk, __fmaf_rn(X.dq[0][R], rtf, X.af[0]), ok);
+        uint32_t k1 = byte_bucket(X.bk, __fmaf_rn(X.dq[1][Gc], rtf, X.af[1]), ok);
+        uint32_t k2 = byte_bucket(X.bk, __fmaf_rn(X.dq[2][B], rtf, X.af[2]), ok);
         if (!ok) {  // near a byte boundary: t~ with the exact roundings, fp64 recovery, exact thresholds
           const double tt = fmin(fmax(__dadd_rn(__dmul_rn(__dmul_rn(bad, A.rqkk), guide_n(N)), __dmul_rn(bbd, A.rqkk)),
                                       A.t_min),
@@ -1409,7 +1368,7 @@ __global__ void __launch_bounds__(kXThreads, 2) k_gx_out(FusedArgs A, int nframe
   __shared__ FusedShared S;
   __shared__ XOutShared X;
   __shared__ PowTables PT;
-  if (MODE == 0) x_out_tables(X, A.thr);
+  if (MODE == 0) byte_buckets_build(X.bk, A.thr);
   if (threadIdx.x < 4) {  // the zero slots of the warp totals (both words, both row parities)
     constexpr int kXBuf2 = 2 * 8 * kXCols + 2 * 8 * kXTw;
     uint64_t* tw = reinterpret_cast<uint64_t*>(dyn + (threadIdx.x >> 1) * kXBuf2) + 2 * kXCols;

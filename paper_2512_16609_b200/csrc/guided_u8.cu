@@ -427,11 +427,8 @@ k_gf_thresholds(const double* __restrict__ part, int nparts, int64_t npx, double
 // shrunk by 1e-6 (one bucket table read per sample); otherwise the exact fp64
 // recovery and threshold walk decide.  Persistent CTAs over the batch's 4-pixel
 // groups; the per-frame tables are rebuilt when a CTA's range enters a new frame.
-constexpr int kApBuckets = 1024;
-constexpr double kApMargin = 1e-6;
 struct ApplyShared {
-  float4 ent[3][kApBuckets + 1];
-  uint8_t k0[3][kApBuckets + 8];
+  ByteBuckets bk[3];
   float dq[3][256];
   double f255[256];
   double thr[3][256];
@@ -447,34 +444,10 @@ __device__ void apply_tables(ApplyShared& S, const double* __restrict__ thr, con
     if (v == 0) S.af[c] = __double2float_rn(airlight[3 * f + c]);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 3 * (kApBuckets + 1); i += blockDim.x) {
-    const int c = i / (kApBuckets + 1), j = i - c * (kApBuckets + 1);
-    const double* T = S.thr[c];
-    const double x = (double)j * (1.0 / kApBuckets);
-    int lo = 0, hi = 255;  // largest k in [0, 255] with k == 0 or T[k] <= x
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (T[mid] <= x) lo = mid;
-      else hi = mid - 1;
-    }
-    auto lo_of = [&](int k) -> float {
-      return k <= 0 ? -INFINITY : (k > 255 ? INFINITY : __double2float_ru(__dadd_rn(T[k], kApMargin)));
-    };
-    auto hi_of = [&](int k) -> float { return k >= 255 ? INFINITY : __double2float_rd(__dsub_rn(T[k + 1], kApMargin)); };
-    S.k0[c][j] = (uint8_t)lo;
-    S.ent[c][j] = make_float4(lo_of(lo), hi_of(lo), lo_of(lo + 1), hi_of(lo + 1));
-  }
+  for (int c = 0; c < 3; ++c) byte_buckets_build(S.bk[c], S.thr[c]);
   __syncthreads();
 }
 
-__device__ __forceinline__ uint32_t apply_byte(const ApplyShared& S, int c, float xf, bool& ok) {
-  const uint32_t j = min(__float2uint_rd(xf * (float)kApBuckets), (uint32_t)kApBuckets);
-  const float4 e = S.ent[c][j];
-  const uint32_t k = S.k0[c][j];
-  const bool in0 = xf >= e.x && xf < e.y, in1 = xf >= e.z && xf < e.w;
-  ok = ok && (in0 || in1);
-  return k + (in1 ? 1u : 0u);
-}
 
 __global__ void __launch_bounds__(256, 3)
 k_gf_apply2(const uint8_t* __restrict__ in, int64_t in_fs, int n, int64_t npx, const double* __restrict__ t_in,
@@ -530,9 +503,9 @@ k_gf_apply2(const uint8_t* __restrict__ in, int64_t in_fs, int n, int64_t npx, c
         float rtf;
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rtf) : "f"(__double2float_rn(t[u])));
         bool ok = true;
-        uint32_t k0 = apply_byte(S, 0, __fmaf_rn(S.dq[0][v0], rtf, S.af[0]), ok);
-        uint32_t k1 = apply_byte(S, 1, __fmaf_rn(S.dq[1][v1], rtf, S.af[1]), ok);
-        uint32_t k2 = apply_byte(S, 2, __fmaf_rn(S.dq[2][v2], rtf, S.af[2]), ok);
+        uint32_t k0 = byte_bucket(S.bk[0], __fmaf_rn(S.dq[0][v0], rtf, S.af[0]), ok);
+        uint32_t k1 = byte_bucket(S.bk[1], __fmaf_rn(S.dq[1][v1], rtf, S.af[1]), ok);
+        uint32_t k2 = byte_bucket(S.bk[2], __fmaf_rn(S.dq[2][v2], rtf, S.af[2]), ok);
         if (!ok) {
           const double rt = __drcp_rn(t[u]);
           k0 = quantize_thr_from(recover_raw(S.f255[v0], A0, t[u], rt), S.thr[0], (int)min(k0, 255u));

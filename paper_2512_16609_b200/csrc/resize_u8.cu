@@ -38,7 +38,7 @@ constexpr int kT1 = 256;            // R1 threads
 constexpr int kT2 = 1024;           // R2 threads
 constexpr int kCap = 4096;          // R2 candidates kept in shared memory
 constexpr int kT3 = 256;            // R3 threads
-constexpr int kColTab = 2048;       // R3: output widths up to this use a column-tap table
+constexpr int kColTab = 1024;       // R3: output widths up to this use a column-tap table
 
 __device__ __forceinline__ double u8f(uint32_t v) { return __ddiv_rn((double)v, 255.0); }
 
@@ -49,7 +49,7 @@ struct Tap {
 };
 __device__ __forceinline__ Tap tap(int i, double scale, int n) {
   double s = __dsub_rn(__dmul_rn(__dadd_rn((double)i, 0.5), scale), 0.5);
-  s = fmin(fmax(s, 0.0), (double)n - 1.0);
+  s = dmin(dmax(s, 0.0), (double)n - 1.0);
   Tap t;
   t.i0 = (int)floor(s);
   t.i1 = min(t.i0 + 1, n - 1);
@@ -89,7 +89,7 @@ __device__ __forceinline__ void resized_rgb_t(const uint8_t* __restrict__ frame,
     } else {
 #pragma unroll
       for (int c = 0; c < 3; ++c)
-        rgb[c] = fmin(__dadd_rn(__dmul_rn(s_f[p00[c]], ty.g), __dmul_rn(s_f[p10[c]], ty.f)), 1.0);
+        rgb[c] = dmin(__dadd_rn(__dmul_rn(s_f[p00[c]], ty.g), __dmul_rn(s_f[p10[c]], ty.f)), 1.0);
     }
     return;
   }
@@ -99,13 +99,46 @@ __device__ __forceinline__ void resized_rgb_t(const uint8_t* __restrict__ frame,
   for (int c = 0; c < 3; ++c) {
     const double r0 = __dadd_rn(__dmul_rn(s_f[p00[c]], ty.g), __dmul_rn(s_f[p10[c]], ty.f));
     const double r1 = __dadd_rn(__dmul_rn(s_f[p01[c]], ty.g), __dmul_rn(s_f[p11[c]], ty.f));
-    rgb[c] = fmin(__dadd_rn(__dmul_rn(r0, tx.g), __dmul_rn(r1, tx.f)), 1.0);
+    rgb[c] = dmin(__dadd_rn(__dmul_rn(r0, tx.g), __dmul_rn(r1, tx.f)), 1.0);
   }
 }
 
 __device__ __forceinline__ void resized_rgb(const uint8_t* __restrict__ frame, const ResizeGeo& G, int y, int x,
                                             const double* __restrict__ s_f, double (&rgb)[3]) {
   resized_rgb_t(frame, G.w, tap(y, G.sy, G.h), tap(x, G.sx, G.w), s_f, rgb);
+}
+
+// Tap with precomputed byte offsets (row: i * 3w, column: 3 i) and both weights.
+struct OffTap {
+  int o0, o1;
+  double f, g;
+};
+__device__ __forceinline__ OffTap off_tap(const Tap& t, int unit) { return OffTap{t.i0 * unit, t.i1 * unit, t.f, t.g}; }
+
+// resized_rgb_t from offset taps (same arithmetic, same zero-weight shortcuts).
+__device__ __forceinline__ void resized_rgb_o(const uint8_t* __restrict__ frame, const OffTap& ty, const OffTap& tx,
+                                              const double* __restrict__ s_f, double (&rgb)[3]) {
+  const uint8_t* p00 = frame + ty.o0 + tx.o0;
+  const uint8_t* p10 = frame + ty.o1 + tx.o0;
+  if (tx.f == 0.0) {
+    if (ty.f == 0.0) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) rgb[c] = s_f[p00[c]];
+    } else {
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        rgb[c] = dmin(__dadd_rn(__dmul_rn(s_f[p00[c]], ty.g), __dmul_rn(s_f[p10[c]], ty.f)), 1.0);
+    }
+    return;
+  }
+  const uint8_t* p01 = frame + ty.o0 + tx.o1;
+  const uint8_t* p11 = frame + ty.o1 + tx.o1;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double r0 = __dadd_rn(__dmul_rn(s_f[p00[c]], ty.g), __dmul_rn(s_f[p10[c]], ty.f));
+    const double r1 = __dadd_rn(__dmul_rn(s_f[p01[c]], ty.g), __dmul_rn(s_f[p11[c]], ty.f));
+    rgb[c] = dmin(__dadd_rn(__dmul_rn(r0, tx.g), __dmul_rn(r1, tx.f)), 1.0);
+  }
 }
 
 __device__ __forceinline__ int bucket_of(double d) { return min(max((int)(d * 4096.0), 0), kResizeBuckets - 1); }
@@ -124,11 +157,11 @@ __device__ __forceinline__ void window_min(const double (&v)[S + 2 * R], double 
 #pragma unroll
   for (int w = 1; w < P; w <<= 1) {
 #pragma unroll
-    for (int i = 0; i + w < N; ++i) m[i] = fmin(m[i], m[i + w]);
+    for (int i = 0; i + w < N; ++i) m[i] = dmin(m[i], m[i + w]);
   }
   // m[i] = min over [i, i + P); the window [i, i + L) = [i, i + P) u [i + L - P, i + L)
 #pragma unroll
-  for (int i = 0; i < S; ++i) o[i] = fmin(m[i], m[i + L - P]);
+  for (int i = 0; i < S; ++i) o[i] = dmin(m[i], m[i + L - P]);
 }
 
 // Tile kernel with the erosion radius fixed at compile time (register windows).
@@ -150,24 +183,32 @@ k_rs_dark_t(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, double* 
   const int f = blockIdx.z;
   const int ty0 = blockIdx.y * kTH, tx0 = blockIdx.x * kTW;
   double* cm = sm;  // [PH][PWP] resized channel minimum (clamped coordinates); then [PH][RP] row minima
-  __shared__ TapS s_ty[PH], s_tx[PW];
+  // tap tables: byte offsets of the two source rows / columns and their weights
+  __shared__ OffTap s_ty[PH], s_tx[PW];
   s_f[threadIdx.x] = u8f(threadIdx.x);
   for (int b = threadIdx.x; b < kHistWords; b += kT1) s_hist[b] = 0;
   for (int k = threadIdx.x; k < PH + PW; k += kT1) {
-    if (k < PH) s_ty[k] = compact(tap(min(max(ty0 - R + k, 0), G.H - 1), G.sy, G.h));
-    else s_tx[k - PH] = compact(tap(min(max(tx0 - R + k - PH, 0), G.W - 1), G.sx, G.w));
+    if (k < PH) s_ty[k] = off_tap(tap(min(max(ty0 - R + k, 0), G.H - 1), G.sy, G.h), 3 * G.w);
+    else s_tx[k - PH] = off_tap(tap(min(max(tx0 - R + k - PH, 0), G.W - 1), G.sx, G.w), 3);
   }
   __syncthreads();
   const uint8_t* frame = in + (int64_t)f * in_fs;
-  // two samples per iteration: both samples' byte loads are in flight together
-  for (int e = threadIdx.x; e < PH * PW; e += 2 * kT1) {
-    const int e2 = min(e + kT1, PH * PW - 1);
-    const int py = e / PW, px = e - py * PW, py2 = e2 / PW, px2 = e2 - py2 * PW;
-    double rgb[3], rgb2[3];
-    resized_rgb_t(frame, G.w, expand(s_ty[py], G.h), expand(s_tx[px], G.w), s_f, rgb);
-    resized_rgb_t(frame, G.w, expand(s_ty[py2], G.h), expand(s_tx[px2], G.w), s_f, rgb2);
-    cm[py * PWP + px] = fmin(fmin(rgb[0], rgb[1]), rgb[2]);  // estimation.py:38
-    if (e + kT1 < PH * PW) cm[py2 * PWP + px2] = fmin(fmin(rgb2[0], rgb2[1]), rgb2[2]);
+  // a thread keeps one tile column (its column tap in registers) and walks the rows, two
+  // at a time so both samples' byte loads are in flight together
+  {
+    constexpr int NRG = kT1 / PW;  // row groups
+    const int px = threadIdx.x % PW, pr = threadIdx.x / PW;
+    if (pr < NRG) {
+      const OffTap cx = s_tx[px];
+      for (int py = pr; py < PH; py += 2 * NRG) {
+        const int py2 = min(py + NRG, PH - 1);
+        double rgb[3], rgb2[3];
+        resized_rgb_o(frame, s_ty[py], cx, s_f, rgb);
+        resized_rgb_o(frame, s_ty[py2], cx, s_f, rgb2);
+        cm[py * PWP + px] = dmin(dmin(rgb[0], rgb[1]), rgb[2]);  // estimation.py:38
+        cm[py2 * PWP + px] = dmin(dmin(rgb2[0], rgb2[1]), rgb2[2]);
+      }
+    }
   }
   __syncthreads();
   // rows first (morphology.py:73): item = (8-column segment, row), lanes on consecutive
@@ -249,14 +290,14 @@ k_rs_dark(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, int r, dou
     const int y = min(max(ty0 - r + py, 0), G.H - 1), x = min(max(tx0 - r + px, 0), G.W - 1);
     double rgb[3];
     resized_rgb(frame, G, y, x, s_f, rgb);
-    cm[e] = fmin(fmin(rgb[0], rgb[1]), rgb[2]);  // estimation.py:38
+    cm[e] = dmin(dmin(rgb[0], rgb[1]), rgb[2]);  // estimation.py:38
   }
   __syncthreads();
   for (int e = threadIdx.x; e < PH * kTW; e += kT1) {  // morphology.py:73: rows first
     const int py = e / kTW, px = e - py * kTW;
     const double* row = cm + py * PW + px;
     double v = row[0];
-    for (int k = 1; k <= 2 * r; ++k) v = fmin(v, row[k]);
+    for (int k = 1; k <= 2 * r; ++k) v = dmin(v, row[k]);
     rm[e] = v;
   }
   __syncthreads();
@@ -267,7 +308,7 @@ k_rs_dark(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, int r, dou
     if (y < G.H && x < G.W) {
       const double* col = rm + py * kTW + px;
       double v = col[0];
-      for (int k = 1; k <= 2 * r; ++k) v = fmin(v, col[k * kTW]);
+      for (int k = 1; k <= 2 * r; ++k) v = dmin(v, col[k * kTW]);
       dark[(int64_t)f * npx + (int64_t)y * G.W + x] = v;
       atomicAdd(&s_hist[bucket_of(v)], 1u);
     }
@@ -509,7 +550,7 @@ k_rs_select(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const do
   }
   if (threadIdx.x < 3) {
     const double mean = __ddiv_rn(acc, (double)K);
-    airlight[3 * f + threadIdx.x] = fmax(__dmul_rn(alpha, mean), 1e-6);
+    airlight[3 * f + threadIdx.x] = dmax(__dmul_rn(alpha, mean), 1e-6);
   }
 }
 
@@ -527,6 +568,7 @@ k_rs_recover(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const d
   __shared__ double red[3][kT3 / 32];
   __shared__ TapS s_tx[kColTab];
   __shared__ PowTables PT;  // balance sums (MODE 1)
+  __shared__ ByteBuckets BK;  // fp32 fast path of the bytes (MODE 0)
   const int f = blockIdx.y;
   s_f[threadIdx.x] = u8f(threadIdx.x);
   if (MODE == 1) pow_tables_init(PT);
@@ -534,9 +576,14 @@ k_rs_recover(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const d
   if (MODE == 2)
     for (int c = 0; c < 3; ++c) s_thr[c][threadIdx.x] = thr[((int64_t)f * 3 + c) * 256 + threadIdx.x];
   __syncthreads();
+  if (MODE == 0) {
+    byte_buckets_build(BK, s_thr[0]);
+    __syncthreads();
+  }
   const double A0 = airlight[3 * f], A1 = airlight[3 * f + 1], A2 = airlight[3 * f + 2];
-  const double amax = fmax(fmax(A0, A1), A2);
+  const double amax = dmax(dmax(A0, A1), A2);
   const double ramax = __drcp_rn(amax);  // cmin / amax as the exact div_rb
+  const float af0 = (float)A0, af1 = (float)A1, af2 = (float)A2;
   const float ig = (float)inv_gamma;
   float g0 = 1.0f, g1 = 1.0f, g2 = 1.0f;
   if (MODE == 2) {
@@ -557,16 +604,38 @@ k_rs_recover(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const d
     const int64_t p = (int64_t)y * G.W + x;
     double rgb[3];
     resized_rgb_t(frame, G.w, tap(y, G.sy, G.h), tab ? expand(s_tx[x], G.w) : tap(x, G.sx, G.w), s_f, rgb);
-    const double cmin = fmin(fmin(rgb[0], rgb[1]), rgb[2]);
-    const double t = fmin(fmax(__dsub_rn(1.0, __dmul_rn(omega, div_rb(cmin, amax, ramax))), t_min), 1.0);
+    const double cmin = dmin(dmin(rgb[0], rgb[1]), rgb[2]);
+    if (MODE == 0) {
+      // fp32 fast path (byte_bucket): t~ to ~1e-16 is plenty for it; the exact t,
+      // recovery and thresholds only for a sample near a byte boundary
+      const double tq = dmin(dmax(__fma_rn(-omega, __dmul_rn(cmin, ramax), 1.0), t_min), 1.0);
+      const float rtf = rcp_approx(__double2float_rn(tq));
+      bool ok = true;
+      uint32_t k0 = byte_bucket(BK, __fmaf_rn(__double2float_rn(__dsub_rn(rgb[0], A0)), rtf, af0), ok);
+      uint32_t k1 = byte_bucket(BK, __fmaf_rn(__double2float_rn(__dsub_rn(rgb[1], A1)), rtf, af1), ok);
+      uint32_t k2 = byte_bucket(BK, __fmaf_rn(__double2float_rn(__dsub_rn(rgb[2], A2)), rtf, af2), ok);
+      if (!ok) {
+        const double t = dmin(dmax(__dsub_rn(1.0, __dmul_rn(omega, div_rb(cmin, amax, ramax))), t_min), 1.0);
+        const double rt = __drcp_rn(t);
+        k0 = quantize_thr_from(recover_raw(rgb[0], A0, t, rt), s_thr[0], (int)k0);
+        k1 = quantize_thr_from(recover_raw(rgb[1], A1, t, rt), s_thr[0], (int)k1);
+        k2 = quantize_thr_from(recover_raw(rgb[2], A2, t, rt), s_thr[0], (int)k2);
+      }
+      uint8_t* o = fo + 3 * p;
+      o[0] = (uint8_t)k0;
+      o[1] = (uint8_t)k1;
+      o[2] = (uint8_t)k2;
+      continue;
+    }
+    const double t = dmin(dmax(__dsub_rn(1.0, __dmul_rn(omega, div_rb(cmin, amax, ramax))), t_min), 1.0);
     const double rt = __drcp_rn(t);
     const double x0 = recover_raw(rgb[0], A0, t, rt), x1 = recover_raw(rgb[1], A1, t, rt),
                  x2 = recover_raw(rgb[2], A2, t, rt);
     if (MODE == 1) {
       if (gamma_is_one) {
-        acc0 = __dadd_rn(acc0, fmin(fmax(x0, 0.0), 1.0));
-        acc1 = __dadd_rn(acc1, fmin(fmax(x1, 0.0), 1.0));
-        acc2 = __dadd_rn(acc2, fmin(fmax(x2, 0.0), 1.0));
+        acc0 = __dadd_rn(acc0, dmin(dmax(x0, 0.0), 1.0));
+        acc1 = __dadd_rn(acc1, dmin(dmax(x1, 0.0), 1.0));
+        acc2 = __dadd_rn(acc2, dmin(dmax(x2, 0.0), 1.0));
       } else {
         acc0 = __dadd_rn(acc0, pow_tab(x0, inv_gamma, PT));
         acc1 = __dadd_rn(acc1, pow_tab(x1, inv_gamma, PT));
