@@ -2,7 +2,8 @@
 
 C5 is 64 x 7680x4320 in image mode with a 31x31 dark-channel patch
 (patch_radius=15), guided radius 60, eps 1e-3 and gray-world balance (the image
-default).  Frames this wide take the wide-frame guided-filter kernels, so they are
+default).  Frames this wide take the default two-pass exact guided filter (and, for guided
+radii above 63 or with DHZ_GUIDED_PATH=strip, the CPT = 4 strip kernels), so they are
 compared with the CPU oracle (reference estimation.py:110-172, pipeline.py:163-216)
 here, on narrow 4096-wide strips of the C5 generator with balance on and off, and
 on one full 7680x4320 C5 frame.
@@ -37,11 +38,16 @@ def _compare(frames, params, oracle):
         assert d.max() <= 1 and int((d > 0).sum()) <= 2, (i, int(d.max()), int((d > 0).sum()))
 
 
+@pytest.mark.parametrize("path", ["default", "strip"])
 @pytest.mark.parametrize("balance", [True, False])
 @pytest.mark.parametrize("width,height", [(4096, 160), (4104, 131)])
-def test_wide_strips(oracle, balance, width, height):
+def test_wide_strips(oracle, monkeypatch, path, balance, width, height):
+    """The default (two-pass exact) filter and the strip kernels (CPT = 4 at this width;
+    the default for guided radii above 63)."""
     from paper_2512_16609_b200.synthetic import make_frames
 
+    if path == "strip":
+        monkeypatch.setenv("DHZ_GUIDED_PATH", "strip")
     frames = make_frames("c5", frames=2, width=width, height=height)
     _compare(frames, _c5_params(white_balance=balance), oracle)
 

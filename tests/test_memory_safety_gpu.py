@@ -11,7 +11,8 @@ closed on the B200 pool this package is tested on):
 * determinism: repeated runs of the same batch are bit-identical (a data race on
   shared memory or on the select/balance counters would show up as flips).
 Each native path is covered: video (vectorised and odd widths, balance), image
-mode (strip kernels and the fused kernel, balance on/off) and the default resize.
+mode (strip kernels, the one-pass and the two-pass exact kernels, balance on/off) and the
+default resize.
 """
 
 import ctypes
@@ -90,14 +91,14 @@ def _run(frames, params, ws_fill, io_fill):
     return fout[G:-G].clone(), fair[G:-G].clone()
 
 
-@pytest.mark.parametrize("path", ["strip", "fused"])
+@pytest.mark.parametrize("path", ["strip", "fused", "twopass"])
 @pytest.mark.parametrize("case", range(8))
 def test_guards_and_poison(monkeypatch, path, case):
     from paper_2512_16609_b200.synthetic import make_frames
 
     name, params, (n, h, w) = _cases()[case]
-    if path == "fused" and params.mode != "image":
-        pytest.skip("fused kernel: image mode only")
+    if path in ("fused", "twopass") and params.mode != "image":
+        pytest.skip("exact guided-filter kernels: image mode only")
     monkeypatch.setenv("DHZ_GUIDED_PATH", path)
     frames = make_frames("c3", frames=n, width=w, height=h, device="cuda")
     ref_out, ref_air = _run(frames, params, 0x00, 0x00)
