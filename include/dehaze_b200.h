@@ -61,12 +61,6 @@ typedef struct dhz_params {
 
 const char* dhz_last_error(void);
 int dhz_abi_version(void);
-/* Host memcpy of `bytes` split over up to `nthreads` native threads of a parked pool
- * (no device involved): process_stream's per-frame staging copies (reference
- * pipeline.py:232-308 takes one host array per frame; the copies into pinned staging
- * and out to fresh arrays bound the stream).  Returns 0, or DHZ_E_INVALID for null
- * pointers with bytes > 0. */
-int dhz_host_copy(void* dst, const void* src, size_t bytes, int nthreads);
 /* Number of visible CUDA devices (>= 1) or DHZ_E_CUDA when there is none. */
 int dhz_device_count(void);
 

@@ -56,7 +56,6 @@ SIGNATURES = {
     "dhz_last_error": (ctypes.c_char_p, []),
     "dhz_abi_version": (_c_int, []),
     "dhz_device_count": (_c_int, []),
-    "dhz_host_copy": (_c_int, [_c_void_p, _c_void_p, _c_size, _c_int]),
     "dhz_frames_u8_workspace": (_c_size, [_c_int, _c_int, _c_int, _P]),
     "dhz_frames_u8": (_c_int, [_c_void_p, _c_i64, _c_int, _c_int, _c_int, _P, _c_void_p, _c_i64,
                                _c_void_p, _c_void_p, _c_size, _c_void_p, _c_void_p]),

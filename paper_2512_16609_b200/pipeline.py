@@ -500,22 +500,33 @@ def dehaze_host_batch(frames, params=None, out=None, airlight=None, chunk=None, 
 
 _STREAM_BATCH_BYTES = 256 << 20   # float path: ~256 MiB of input frames per device launch
 _COPY_THREADS = max(1, min(8, (__import__("os").cpu_count() or 1)))
+_copy_pool = None
+
+
+def _pool():
+    """Host-copy threads of process_stream (numpy/torch copies release the GIL)."""
+    global _copy_pool
+    if _copy_pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _copy_pool = ThreadPoolExecutor(max_workers=_COPY_THREADS, thread_name_prefix="dhz-copy")
+    return _copy_pool
 
 
 def _par_copy(dst, src):
-    """dst.copy_(src) for contiguous host tensors of the same size, split over the
-    library's native copy threads (dhz_host_copy: parked workers, a call costs a
-    wake-up, so 1080p frames gain too); returns when the copy is complete."""
-    from . import _native
-
+    """dst.copy_(src) for host tensors, split over the copy threads when large; returns
+    when the copy is complete."""
     nb = src.numel() * src.element_size()
-    if nb < (1 << 20) or not (dst.is_contiguous() and src.is_contiguous()) or dst.numel() != src.numel():
+    # measured on the B200 box's host (tools/stream_copy_probe.py): splitting a 6 MB 1080p
+    # frame over threads loses to one memcpy (dispatch cost); 4K/8K frames gain
+    k = min(_COPY_THREADS, nb >> 22) if nb >= (8 << 20) else 1  # >= 4 MiB per piece
+    if k < 2:
         dst.copy_(src)
         return
-    _native.check(_native.load_library().dhz_host_copy(dst.data_ptr(), src.data_ptr(), nb, _COPY_THREADS),
-                  "dhz_host_copy")
-
-
+    d, s_ = dst.reshape(-1), src.reshape(-1)
+    n = d.numel()
+    cuts = [n * i // k for i in range(k + 1)]
+    list(_pool().map(lambda i: d[cuts[i]:cuts[i + 1]].copy_(s_[cuts[i]:cuts[i + 1]]), range(k)))
 _STREAM_BATCH_MAX = 256
 _PIPE_BATCH_BYTES = 48 << 20      # native path: input bytes per pipelined batch
 _PIPE_SLOTS = 3
@@ -621,8 +632,11 @@ class _StreamPipe:
         if self.fresh:  # the sink may keep them: fresh arrays, filled by the copy threads
             outs = [np.empty(self.out_shape, dtype=np.uint8) for _ in range(m)]
             hout = self.hout[s]
-            for i in range(m):  # native copy threads per frame (first touch of the fresh pages included)
-                _par_copy(torch.from_numpy(outs[i]), hout[i])
+            if m > 1 and outs[0].nbytes >= (1 << 19):
+                list(_pool().map(lambda i: torch.from_numpy(outs[i]).copy_(hout[i]), range(m)))
+            else:
+                for i in range(m):
+                    torch.from_numpy(outs[i]).copy_(hout[i])
         else:
             outs = [self.hout[s][i].numpy() for i in range(m)]
         for i in range(m):

@@ -3,8 +3,6 @@ import ctypes
 import os
 import re
 
-import pytest
-
 from paper_2512_16609_b200 import _native
 
 HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "dehaze_b200.h")
@@ -51,28 +49,3 @@ def test_batch_limit_rejected_without_a_device():
     assert lib.dhz_frames_u8_workspace(MAX_FRAMES_PER_CALL, 4, 4, ctypes.byref(p)) > 0
     assert lib.dhz_frames_u8_workspace(MAX_FRAMES_PER_CALL + 1, 4, 4, ctypes.byref(p)) == 0
     assert b"split the batch" in lib.dhz_last_error()
-
-
-@pytest.mark.parametrize("nbytes", [0, 1, 4095, 1 << 20, (6 << 20) + 13, 25 << 20])
-@pytest.mark.parametrize("threads", [1, 3, 8, 64])
-def test_host_copy(nbytes, threads):
-    """dhz_host_copy (host-only, no device): byte-exact for any size and thread count."""
-    import numpy as np
-
-    from paper_2512_16609_b200 import _native
-
-    lib = _native.load_library()
-    rng = np.random.default_rng(nbytes + threads)
-    src = rng.integers(0, 256, size=max(nbytes, 1), dtype=np.uint8)
-    dst = np.zeros_like(src)
-    assert lib.dhz_host_copy(dst.ctypes.data, src.ctypes.data, nbytes, threads) == 0
-    assert np.array_equal(dst[:nbytes], src[:nbytes])
-    assert not dst[nbytes:].any()
-
-
-def test_host_copy_rejects_null():
-    from paper_2512_16609_b200 import _native
-
-    lib = _native.load_library()
-    assert lib.dhz_host_copy(None, None, 16, 4) == _native.DHZ_E_INVALID
-    assert lib.dhz_host_copy(None, None, 0, 4) == 0

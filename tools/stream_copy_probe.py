@@ -1,5 +1,5 @@
-"""process_stream host-copy variants on C3 frames: native copy threads (dhz_host_copy via
-pipeline._par_copy) for the input staging and the fresh output arrays, 1..16 threads."""
+"""process_stream host-copy variants on C3 frames: copy threads on/off for the input
+staging and the fresh output arrays (pipeline._COPY_THREADS, _par_copy)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -14,6 +14,7 @@ p = DehazeParams(resize_to=None)
 orig_par = pipeline._par_copy
 for threads in (1, 2, 4, 8, 16):
     pipeline._COPY_THREADS = threads
+    pipeline._copy_pool = None
     for keep in (False, True):
         got = []
         sink = got.append if keep else (lambda o: None)
