@@ -1155,8 +1155,7 @@ __device__ __forceinline__ void xwin4(const U* __restrict__ E, const U* __restri
 // Pass 2 over output rows [y0, y1) of one strip: box of (a_q, b_q) -> t~ -> output.
 template <int MODE, int R4>
 __device__ __forceinline__ void x_out_segment(const FusedArgs& A, const FusedShared& S, const XOutShared& X,
-                                              const PowTables& PT, unsigned char* dyn, int f, int strip, int y0, int y1,
-                                              unsigned long long* __restrict__ bsum3) {
+                                              unsigned char* dyn, int f, int strip, int y0, int y1) {
   constexpr int LOFF = (4 - R4) & 3, HOFF = (R4 + 1) & 3;
   const int r = A.r, H = A.H, W = A.W;
   const int t = threadIdx.x;
@@ -1307,11 +1306,7 @@ __device__ __forceinline__ void x_out_segment(const FusedArgs& A, const FusedSha
       } else {
         const double tt =
             fmin(fmax(__dadd_rn(__dmul_rn(__dmul_rn(bad, A.rqkk), guide_n(N)), __dmul_rn(bbd, A.rqkk)), A.t_min), 1.0);
-        tv[c] = tt;
-        const double rt = __drcp_rn(tt);
-        bs0 += gw_term(S.f255[R], A0, rt, A, PT) - kGwBias;
-        bs1 += gw_term(S.f255[Gc], A1, rt, A, PT) - kGwBias;
-        bs2 += gw_term(S.f255[B], A2, rt, A, PT) - kGwBias;
+        tv[c] = tt;  // the gray-world sums and the bytes follow in k_gw_sums / k_gf_apply2
       }
     }
     if (MODE == 1) {  // t~ for the apply pass, 32 bytes per thread
@@ -1351,15 +1346,6 @@ __device__ __forceinline__ void x_out_segment(const FusedArgs& A, const FusedSha
   }
   if (y < y1) step(std::integral_constant<int, 0>{}, y);
 #undef CL
-  if (MODE == 1) {  // per-frame channel sums (integer: order-free)
-    unsigned long long v[3] = {bs0, bs1, bs2};
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v[ch] += __shfl_xor_sync(0xffffffffu, v[ch], o);
-      if ((threadIdx.x & 31) == 0 && v[ch]) atomicAdd(&bsum3[ch], v[ch]);
-    }
-  }
 }
 
 template <int MODE>
@@ -1367,7 +1353,6 @@ __global__ void __launch_bounds__(kXThreads, 2) k_gx_out(FusedArgs A, int nframe
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ FusedShared S;
   __shared__ XOutShared X;
-  __shared__ PowTables PT;
   if (MODE == 0) byte_buckets_build(X.bk, A.thr);
   if (threadIdx.x < 4) {  // the zero slots of the warp totals (both words, both row parities)
     constexpr int kXBuf2 = 2 * 8 * kXCols + 2 * 8 * kXTw;
@@ -1379,7 +1364,6 @@ __global__ void __launch_bounds__(kXThreads, 2) k_gx_out(FusedArgs A, int nframe
     S.f255[v] = __ddiv_rn((double)v, 255.0);
     S.thr2[v] = make_double2(v == 0 ? -INFINITY : A.thr[v], v == 255 ? INFINITY : A.thr[v + 1]);
   }
-  if (MODE == 1 && !A.gamma_is_one) pow_tables_init(PT, e);
   const int64_t cols = (int64_t)nframes * A.nstrips;
   const int64_t total = cols * A.H;
   const int64_t b0 = total * blockIdx.x / gridDim.x, b1 = total * (blockIdx.x + 1) / gridDim.x;
@@ -1402,11 +1386,80 @@ __global__ void __launch_bounds__(kXThreads, 2) k_gx_out(FusedArgs A, int nframe
     }
     __syncthreads();
     switch (A.r & 3) {
-      case 0: x_out_segment<MODE, 0>(A, S, X, PT, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
-      case 1: x_out_segment<MODE, 1>(A, S, X, PT, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
-      case 2: x_out_segment<MODE, 2>(A, S, X, PT, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
-      default: x_out_segment<MODE, 3>(A, S, X, PT, dyn, f, strip, yseg0, yseg1, A.bsum + 3 * f); break;
+      case 0: x_out_segment<MODE, 0>(A, S, X, dyn, f, strip, yseg0, yseg1); break;
+      case 1: x_out_segment<MODE, 1>(A, S, X, dyn, f, strip, yseg0, yseg1); break;
+      case 2: x_out_segment<MODE, 2>(A, S, X, dyn, f, strip, yseg0, yseg1); break;
+      default: x_out_segment<MODE, 3>(A, S, X, dyn, f, strip, yseg0, yseg1); break;
     }
+  }
+}
+
+// Gray-world channel sums of the two-pass form, a streaming pass over t~ and the frame:
+// per pixel the three gw_term values (the same function as the one-pass kernel's
+// inline sums, exact integer totals, so the same per-frame sums), kept out of the
+// box-filter kernel whose register file and shared memory they would share.
+// Persistent CTAs over the batch's 4-pixel groups, per-frame u64 totals by atomics.
+__global__ void __launch_bounds__(256) k_gw_sums(FusedArgs A, int n, int64_t npx) {
+  __shared__ PowTables PT;
+  __shared__ double s_f[256];
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) s_f[v] = __ddiv_rn((double)v, 255.0);
+  if (!A.gamma_is_one) pow_tables_init(PT, A.inv_gamma);
+  __syncthreads();
+  const int64_t G = (npx + 3) >> 2;
+  const int64_t total = (int64_t)n * G;
+  const int64_t g0 = total * blockIdx.x / gridDim.x, g1 = total * (blockIdx.x + 1) / gridDim.x;
+  const bool vec = (npx & 3) == 0 && (A.in_fs & 3) == 0 && ((uintptr_t)A.in & 3) == 0 &&
+                   ((uintptr_t)A.t_out & 15) == 0;
+  for (int64_t s0 = g0; s0 < g1;) {
+    const int f = (int)(s0 / G);
+    const int64_t s1 = min(g1, (int64_t)(f + 1) * G);
+    const double A0 = A.airlight[3 * f], A1 = A.airlight[3 * f + 1], A2 = A.airlight[3 * f + 2];
+    const uint8_t* fi = A.in + (int64_t)f * A.in_fs;
+    const double* ft = A.t_out + (int64_t)f * npx;
+    unsigned long long b0 = 0, b1 = 0, b2 = 0;
+    for (int64_t g = s0 + threadIdx.x; g < s1; g += blockDim.x) {
+      const int64_t p0 = (g - (int64_t)f * G) * 4;
+      const int np = (int)min((int64_t)4, npx - p0);
+      double t[4];
+      uint32_t w[3];
+      if (vec) {
+        const double2 ta = *reinterpret_cast<const double2*>(ft + p0);
+        const double2 tb = *reinterpret_cast<const double2*>(ft + p0 + 2);
+        t[0] = ta.x; t[1] = ta.y; t[2] = tb.x; t[3] = tb.y;
+        const uint32_t* q = reinterpret_cast<const uint32_t*>(fi + 3 * p0);
+        w[0] = __ldg(q); w[1] = __ldg(q + 1); w[2] = __ldg(q + 2);
+      } else {
+        uint32_t bb[12];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t p = p0 + min(u, np - 1);
+          t[u] = ft[p];
+          bb[3 * u] = fi[3 * p];
+          bb[3 * u + 1] = fi[3 * p + 1];
+          bb[3 * u + 2] = fi[3 * p + 2];
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) w[q] = bb[4 * q] | (bb[4 * q + 1] << 8) | (bb[4 * q + 2] << 16) | (bb[4 * q + 3] << 24);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (u >= np) break;
+        uint32_t R, Gc, B;
+        rgb_of(w, u, R, Gc, B);
+        const double rt = __drcp_rn(t[u]);
+        b0 += gw_term(s_f[R], A0, rt, A, PT) - kGwBias;
+        b1 += gw_term(s_f[Gc], A1, rt, A, PT) - kGwBias;
+        b2 += gw_term(s_f[B], A2, rt, A, PT) - kGwBias;
+      }
+    }
+    unsigned long long v[3] = {b0, b1, b2};
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[ch] += __shfl_xor_sync(0xffffffffu, v[ch], o);
+      if ((threadIdx.x & 31) == 0 && v[ch]) atomicAdd(&A.bsum[3 * f + ch], v[ch]);
+    }
+    s0 = s1;
   }
 }
 
@@ -1641,6 +1694,12 @@ cudaError_t guided_x_u8(const uint8_t* in, int64_t in_fs, int n, int H, int W, i
     if ((e = cudaMemsetAsync(bsum, 0, 24ull * c, st)) != cudaSuccess) return e;
     k_gx_out<1><<<P.ctas, kXThreads, kXSmem2, st>>>(A, c);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    {
+      const int64_t groups = (int64_t)c * ((npx + 3) / 4);
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(4LL * sms, (groups + 255) / 256));
+      k_gw_sums<<<grid, 256, 0, st>>>(A, c, npx);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     k_bsum_to_part<<<(3 * c + 255) / 256, 256, 0, st>>>(bsum, c, part);
     if ((e = balance_thresholds(part, 1, c, npx, gamma, bthr, gains, st)) != cudaSuccess) return e;
     if ((e = guided_apply(A.in, in_fs, c, npx, tmap, A.airlight, bthr, gains, gamma, A.out, out_fs, st)) !=
