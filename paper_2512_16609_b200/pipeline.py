@@ -547,7 +547,7 @@ class _StreamPipe:
     last A' (an event chain across the slots; the carry hops devices if needed).
     """
 
-    def __init__(self, devs, params, shape, fresh=True, stabilise=None):
+    def __init__(self, devs, params, shape, fresh=True, stabilise=None, n_hint=None):
         import torch
 
         from .engine import FrameEngine
@@ -555,6 +555,8 @@ class _StreamPipe:
         H, W, _ = shape
         OH, OW = FrameEngine.working_size(params, H, W)
         self.batch = max(1, min(_STREAM_BATCH_MAX, _PIPE_BATCH_BYTES // (3 * H * W)))
+        if n_hint is not None:  # a short clip of known length: slots no larger than its share
+            self.batch = max(1, min(self.batch, -(-int(n_hint) // _PIPE_SLOTS)))
         self.params = params
         self.lam = stabilise
         self.out_shape = (OH, OW, 3)
@@ -673,6 +675,10 @@ def process_stream(frames, params=None, sink=None, workers=1, devices=None, stab
     lam = _check_stabilise(stabilise)
     devs = _device_list(devices)
 
+    try:  # a sequence of known length sizes the pipelined batches of a short clip
+        n_hint = len(frames)
+    except TypeError:
+        n_hint = None
     trace = []
     count = 0
     expected_shape = None
@@ -723,7 +729,8 @@ def process_stream(frames, params=None, sink=None, workers=1, devices=None, stab
                 per = frame.nbytes
                 limit = max(1, min(_STREAM_BATCH_MAX, _STREAM_BATCH_BYTES // max(per, 1)))
                 if _native_ok(params, frame.shape[0], frame.shape[1]):
-                    pipe = _StreamPipe(devs if devs is not None else [dev], params, frame.shape, stabilise=lam)
+                    pipe = _StreamPipe(devs if devs is not None else [dev], params, frame.shape, stabilise=lam,
+                                       n_hint=n_hint)
                 elif devs is not None or lam is not None:
                     raise ValueError("devices= / stabilise= need a call the batched native pipeline covers "
                                      "(see _native_ok)")
