@@ -412,6 +412,23 @@ k_gf_thresholds(const double* __restrict__ part, int nparts, int64_t npx, double
     return;
   }
   long long lo = 0, hi = __double_as_longlong(1.0);  // byte(lo) < k <= byte(hi)
+  {
+    // bracket the answer around the analytic inverse x0 = ((k - 1/2)/255 / gain)^gamma
+    // (+- 4096 ulps, verified): ~14 bisection steps instead of ~62 (the full bisection
+    // remains the fallback when the bracket does not hold the step)
+    const double y = __ddiv_rn((double)k - 0.5, 255.0);
+    const double g = copy ? y : __ddiv_rn(y, gain);
+    const double x0 = gamma_is_one ? g : pow(g, __drcp_rn(inv_gamma));
+    if (x0 > 0.0 && x0 < 1.0) {
+      const long long b0 = __double_as_longlong(x0);
+      const long long l = max(b0 - 4096, 0LL), h = min(b0 + 4096, __double_as_longlong(1.0));
+      if (balanced_byte(__longlong_as_double(l), inv_gamma, gamma_is_one, gain, copy) < k &&
+          balanced_byte(__longlong_as_double(h), inv_gamma, gamma_is_one, gain, copy) >= k) {
+        lo = l;
+        hi = h;
+      }
+    }
+  }
   while (hi - lo > 1) {
     const long long mid = lo + (hi - lo) / 2;
     if (balanced_byte(__longlong_as_double(mid), inv_gamma, gamma_is_one, gain, copy) >= k) hi = mid;
