@@ -240,9 +240,6 @@ __device__ __forceinline__ double pow_tab(double x, double e, const PowTables& T
   return q * T.e2[ki & 63] * __longlong_as_double((long long)((ki >> 6) + 1023) << 52);
 }
 
-// ((x - A) / t) + A without the final clip: where the value only feeds the byte
-// thresholds (x < 0 -> byte 0, x > 1 -> the byte of 1) or pow_tab (0 / 1 outside
-// (0, 1)), clipping first gives the same result, so the clip is skipped there.
 // ---- fp32 fast path of an output byte ----------------------------------------------
 // The exact byte of a recovered sample x is #{k >= 1 : thr[k] <= x} (thr[1..255], from
 // the host's np.power, quant.py, or per frame with gray-world gains).  A caller forms xf,
@@ -303,6 +300,9 @@ __device__ __forceinline__ float rcp_approx(float t) {
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
 __device__ __forceinline__ double dmax(double a, double b) { return b > a ? b : a; }
 
+// ((x - A) / t) + A without the final clip: where the value only feeds the byte
+// thresholds (x < 0 -> byte 0, x > 1 -> the byte of 1) or pow_tab (0 / 1 outside
+// (0, 1)), clipping first gives the same result, so the clip is skipped there.
 __device__ __forceinline__ double recover_raw(double x, double A, double t, double rt) {
   return __dadd_rn(div_rb(__dsub_rn(x, A), t, rt), A);
 }

@@ -91,13 +91,13 @@ __device__ __forceinline__ double guide_n(uint32_t N) {
 __device__ __noinline__ double pow_general_ool(double x, double e) { return pow(x, e); }
 
 // Tables of pow_series (gray-world sums only).
-struct PowTables {
+struct SeriesTables {
   double ce[1024];  // c_j^e, c_j = 1 + (j + 0.5)/1024
   double ri[1024];  // RN(1 / c_j)
   double p2[65];    // 2^(-k e)
 };
 
-__device__ __forceinline__ void pow_tables_init(PowTables& T, double e) {
+__device__ __forceinline__ void series_tables_init(SeriesTables& T, double e) {
   for (int j = threadIdx.x; j < 1024; j += blockDim.x) {
     const double c = 1.0 + ((double)j + 0.5) / 1024.0;
     T.ce[j] = pow(c, e);
@@ -110,7 +110,7 @@ __device__ __forceinline__ void pow_tables_init(PowTables& T, double e) {
 // m's 1/1024 interval, m^e = c_j^e (1 + u)^e with |u| < 2^-11 and the binomial series
 // to degree 4 (the u^5 term is below |C(e,5)| 2^-55: 3e-19 relative at e = 1/1.2,
 // 1e-13 at e = 16).  Gray-world channel sums only (bytes never come from it).
-__device__ __forceinline__ double pow_series(double x, const FusedArgs& A, const PowTables& S) {
+__device__ __forceinline__ double pow_series(double x, const FusedArgs& A, const SeriesTables& S) {
   if (!(x > 0.0)) return 0.0;
   if (x >= 1.0) return 1.0;
   const long long bits = __double_as_longlong(x);
@@ -133,7 +133,7 @@ __device__ __forceinline__ double pow_series(double x, const FusedArgs& A, const
 // conversion instruction).
 constexpr unsigned long long kGwBias = 0x4338000000000000ull;
 __device__ __forceinline__ unsigned long long gw_term(double f255v, double Ac, double rt, const FusedArgs& A,
-                                                      const PowTables& PT) {
+                                                      const SeriesTables& PT) {
   const double x = fmin(fmax(__fma_rn(__dsub_rn(f255v, Ac), rt, Ac), 0.0), 1.0);
   const double g = A.gamma_is_one ? x : (A.pow_general ? pow_general_ool(x, A.inv_gamma) : pow_series(x, A, PT));
   return (unsigned long long)__double_as_longlong(__fma_rn(g, 0x1p38, 0x1.8p52));
@@ -451,7 +451,7 @@ constexpr size_t kFusedSmem = (size_t)64 * kFMaxCols + 8 * 8 * kTw + 8ull * kPri
 // One segment: output rows [y0, y1) of strip `strip` of frame f.  R4 = r & 3 fixes the
 // alignment of the window reads.
 template <bool CLIP, int MODE, int R4>
-__device__ __noinline__ void fused_segment(const FusedArgs& A, FusedShared& S, const PowTables& PT, unsigned char* dyn,
+__device__ __noinline__ void fused_segment(const FusedArgs& A, FusedShared& S, const SeriesTables& PT, unsigned char* dyn,
                                            int f, int strip,
                                            int y0, int y1, const FrameConst K, long long* __restrict__ edge,
                                            unsigned long long* __restrict__ bsum3) {
@@ -746,13 +746,13 @@ template <int MODE>
 __global__ void __maxnreg__(168) k_gf_fused(FusedArgs A, int nframes) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ FusedShared S;
-  __shared__ PowTables PT;
+  __shared__ SeriesTables PT;
   const double e = A.inv_gamma;
   for (int v = threadIdx.x; v < 256; v += blockDim.x) {
     S.f255[v] = __ddiv_rn((double)v, 255.0);
     S.thr2[v] = make_double2(v == 0 ? -INFINITY : A.thr[v], v == 255 ? INFINITY : A.thr[v + 1]);
   }
-  if (MODE == 1 && !A.gamma_is_one) pow_tables_init(PT, e);
+  if (MODE == 1 && !A.gamma_is_one) series_tables_init(PT, e);
   const int64_t cols = (int64_t)nframes * A.nstrips;
   const int64_t total = cols * A.H;
   const int64_t b0 = total * blockIdx.x / gridDim.x, b1 = total * (blockIdx.x + 1) / gridDim.x;
@@ -1400,10 +1400,10 @@ __global__ void __launch_bounds__(kXThreads, 2) k_gx_out(FusedArgs A, int nframe
 // box-filter kernel whose register file and shared memory they would share.
 // Persistent CTAs over the batch's 4-pixel groups, per-frame u64 totals by atomics.
 __global__ void __launch_bounds__(256) k_gw_sums(FusedArgs A, int n, int64_t npx) {
-  __shared__ PowTables PT;
+  __shared__ SeriesTables PT;
   __shared__ double s_f[256];
   for (int v = threadIdx.x; v < 256; v += blockDim.x) s_f[v] = __ddiv_rn((double)v, 255.0);
-  if (!A.gamma_is_one) pow_tables_init(PT, A.inv_gamma);
+  if (!A.gamma_is_one) series_tables_init(PT, A.inv_gamma);
   __syncthreads();
   const int64_t G = (npx + 3) >> 2;
   const int64_t total = (int64_t)n * G;
