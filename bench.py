@@ -291,8 +291,13 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    # DHZ_BENCH_SHARDED=1 takes the N>1 code path (process group, dehaze_sharded steps) in a
+    # world of one, so the path can be exercised on a one-GPU lease under torchrun
+    sharded = world > 1 or os.environ.get("DHZ_BENCH_SHARDED") == "1"
+    if sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
 
     from paper_2512_16609_b200.engine import engine_for
     from paper_2512_16609_b200.pipeline import DehazeParams, dehaze_host_batch
@@ -329,7 +334,7 @@ def main():
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
 
     graph = None
-    if native and not args.no_graph and world == 1:
+    if native and not args.no_graph and not sharded:
         # the batch pipeline captured once as a CUDA graph and replayed per step
         # (same kernels on the same buffers; removes the per-launch gaps)
         from paper_2512_16609_b200.engine import GraphedPipeline
@@ -341,14 +346,25 @@ def main():
         graph = GraphedPipeline(frames, params, out=out, airlight=air, streams=1)
         graph_st = GraphedPipeline(frames, params, out=out, airlight=air, streams=1, events=graph_ev)
 
+    shard_pipe = None
+    if sharded and native and not args.no_graph:
+        # the product's multi-GPU path with its two halves captured as CUDA graphs
+        from paper_2512_16609_b200.distributed import ShardedPipeline
+
+        shard_pipe = ShardedPipeline(frames, params, n * world)
+
     def step(ev=None):
         nonlocal out, air
-        if world > 1:
+        if sharded:
             # the product's multi-GPU path: airlight half on this rank's shard, NCCL
-            # all-gather of the trace (24 B/frame), recovery half (distributed.dehaze_sharded)
-            from paper_2512_16609_b200.distributed import dehaze_sharded
+            # all-gather of the trace (24 B/frame), recovery half (distributed.dehaze_sharded
+            # / ShardedPipeline)
+            if shard_pipe is not None:
+                out, _trace = shard_pipe.step()
+            else:
+                from paper_2512_16609_b200.distributed import dehaze_sharded
 
-            out, _trace = dehaze_sharded(frames, params, n * world)
+                out, _trace = dehaze_sharded(frames, params, n * world)
             if ev is not None:
                 for e in ev:
                     e.record(stream)
@@ -366,7 +382,7 @@ def main():
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if sharded:
         dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -378,7 +394,7 @@ def main():
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    if world > 1:
+    if sharded:
         dist.barrier()
     if flush is None:  # inputs larger than L2: back-to-back steps, one event pair
         t_start.record(stream)
@@ -398,7 +414,7 @@ def main():
         torch.cuda.synchronize()
         ms = sum(a.elapsed_time(b) for a, b in pairs)
     clk = clocks.stop()
-    if world > 1:
+    if sharded:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -419,9 +435,22 @@ def main():
             for i in range(n_ev - 1):
                 stage_ms[i] += graph_ev[i].elapsed_time(graph_ev[i + 1]) / args.steps
     else:
+        if sharded and native:
+            # sharded steps carry no stage events (two halves around a collective): the stage
+            # times come from eager runs of the same kernels over this rank's shard, after
+            # the timed region
+            for k in range(args.steps):
+                if flush is not None:
+                    flush.add_(1)
+                eng.run(frames, params, out=out, airlight=air, stream=stream, events=evs[k])
+            torch.cuda.synchronize()
         for k in range(args.steps):
             for i in range(n_ev - 1):
                 stage_ms[i] += evs[k][i].elapsed_time(evs[k][i + 1]) / args.steps
+    if sharded:  # the roofline's launch time is the slowest rank's
+        t = torch.tensor(stage_ms, device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        stage_ms = [float(v) for v in t.tolist()]
     peak, peak_kind = _peaks()
     pipe_bytes = ALG_BYTES[cfg] * n * npx
     pipe_gbs = pipe_bytes / (ms_step / 1000.0) / 1e9
@@ -476,14 +505,14 @@ def main():
         host_air = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
         dehaze_host_batch(host_in, params, out=host_out, airlight=host_air)   # warm-up
         torch.cuda.synchronize()
-        if world > 1:
+        if sharded:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             dehaze_host_batch(host_in, params, out=host_out, airlight=host_air)
         torch.cuda.synchronize()
         el = (time.perf_counter() - t0) / args.e2e_steps
-        if world > 1:
+        if sharded:
             t = torch.tensor([el], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
@@ -509,7 +538,7 @@ def main():
         for _ in range(args.e2e_steps):
             st_ = process_stream(frames_np, params, sink=sink)
         el_s = (time.perf_counter() - t0) / args.e2e_steps
-        if world > 1:
+        if sharded:
             t = torch.tensor([el_s], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el_s = float(t.item())
@@ -548,7 +577,11 @@ def main():
                        "step": ("one CUDA-graph replay of the batch pipeline (no instrumentation in the "
                                 "timed graph; stage times from the same pipeline captured with stage-event "
                                 "nodes, replayed --steps times after the timed region)"
-                                if graph is not None else "eager launches of the batch pipeline"),
+                                if graph is not None else
+                                "airlight half (CUDA graph), NCCL all-gather of the airlight trace (eager), "
+                                "recovery half (CUDA graph) (distributed.ShardedPipeline); stage times from eager runs of the same kernels "
+                                "after the timed region, max over ranks" if sharded else
+                                "eager launches of the batch pipeline"),
                        "l2": (f"inputs + outputs {in_out_bytes / 1e9:.2f} GB/step > 2x the 126 MB L2 "
                               "(no flush needed)" if flush is None else
                               f"inputs + outputs {in_out_bytes / 1e6:.1f} MB/step fit in L2: a 512 MB buffer "
@@ -575,7 +608,7 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 

@@ -17,12 +17,51 @@
 //    max over each 16-row x 32-column unit (unit_max[], from per-item maxima)
 //    and per frame (frame_max[]) that let the top-K select skip units that cannot
 //    hold selected pixels.
+#include <cuda.h>  // CUtensorMap (types only; the encoder is fetched through the runtime)
+
+#include <cstdlib>
+
 #include "dhz_common.cuh"
 #include "dhz_internal.h"
 
 namespace dhz {
 
 namespace {
+
+// ---- TMA row staging (DHZ_K1_TMA=1) ----
+// Each warp owns one 1,536-byte stage and one mbarrier: lane 0 issues a
+// cp.async.bulk.tensor (3-D map over [frame][row][3W/8 x u64]) for the warp's next row
+// right after the current row has been copied from the stage into registers, so the
+// stage plus the registers form the double buffer the LDG variant keeps in registers
+// alone.  Out-of-frame bytes arrive as zeros and are replaced by the all-ones neutral.
+constexpr int kTmaRowBytes = 1536;  // 32 lanes x 48 B (512 pixels)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_row(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(b))
+      : "memory");
+}
 
 constexpr int kTW = kBandW;  // output columns per tile (30 lanes x 16 px)
 constexpr int kBH = 64;    // output rows per tile
@@ -40,6 +79,8 @@ struct RowGeo {
   static constexpr int HPR = (R + 1) / 2;        // neighbour pairs borrowed each side
   static constexpr int NP = 2 * HPR + 8 + 1;     // local pairs (+1 neutral pad)
   static constexpr size_t SMEM = (size_t)ROWS * kTW;
+  static constexpr size_t STAGE_OFF = (SMEM + 127) / 128 * 128;  // TMA stages behind the row minima
+  static constexpr size_t SMEM_TMA = STAGE_OFF + (size_t)(256 / 32) * kTmaRowBytes;
 };
 
 // Pipe balance.  Both passes are bound by the integer ALU pipe (~90 % busy in ncu,
@@ -94,13 +135,14 @@ __device__ __forceinline__ uint32_t vert_final(const uint32_t (&v)[N], int j) {
   return min3(v[j], v[j + P], v[j + L - P]);
 }
 
-template <int R>
+template <int R, bool TMA>
 __global__ void __launch_bounds__(kThreads, R <= 8 ? DHZ_K1_MINB : 1)
 k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t* __restrict__ dark,
-            int64_t dark_fs, uint32_t* __restrict__ frame_max, uint32_t* __restrict__ unit_max) {
+            int64_t dark_fs, uint32_t* __restrict__ frame_max, uint32_t* __restrict__ unit_max,
+            const __grid_constant__ CUtensorMap tmap) {
   using G = RowGeo<R>;
   constexpr int L = G::L, P = G::P, HPR = G::HPR, NP = G::NP;
-  extern __shared__ __align__(16) uint8_t hrow[];  // [ROWS][kTW] horizontal minima
+  extern __shared__ __align__(128) uint8_t hrow[];  // [ROWS][kTW] horizontal minima (+ TMA stages)
   const int f = blockIdx.z;
   const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kBH;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -125,11 +167,53 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
     }
     src_row += pitch8;
   };
+  // TMA variant: the warp's stage and barrier; issue_row(v) arms the barrier and starts
+  // the bulk copy of row v (rows outside the frame are not fetched)
+  __shared__ __align__(8) uint64_t s_mbar[kThreads / 32];
+  uint8_t* stage = hrow + G::STAGE_OFF + (size_t)warp * kTmaRowBytes;
+  uint64_t* mbar = &s_mbar[warp];
+  uint32_t parity = 0;
+  auto row_ok = [&](int v) {
+    const int y = y0 - R + v;
+    return v < G::ROWS && y >= 0 && y < H;
+  };
+  auto issue_row = [&](int v) {
+    if (lane == 0 && row_ok(v)) {
+      mbar_expect_tx(mbar, kTmaRowBytes);
+      tma_load_row(stage, &tmap, (x0 - 16) * 3 / 8, y0 - R + v, f, mbar);
+    }
+  };
+  if (TMA) {
+    if (lane == 0) {
+      mbar_init(mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncwarp();
+    issue_row(warp);
+  }
   uint4 na, nb, nd;
-  load_row(warp, na, nb, nd);
+  if (!TMA) load_row(warp, na, nb, nd);
   for (int v = warp; v < G::ROWS; v += kThreads / 32) {
-    const uint4 a = na, b = nb, d = nd;
-    load_row(v + kThreads / 32, na, nb, nd);
+    uint4 a, b, d;
+    if (TMA) {
+      a = b = d = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+      if (row_ok(v)) {  // warp-uniform
+        mbar_wait(mbar, parity);
+        parity ^= 1;
+        if (col_ok) {
+          const uint4* sp = reinterpret_cast<const uint4*>(stage + 48 * lane);
+          a = sp[0];
+          b = sp[1];
+          d = sp[2];
+        }
+      }
+      __syncwarp();  // every lane has read the stage before it is refilled
+      issue_row(v + kThreads / 32);
+    } else {
+      a = na, b = nb, d = nd;
+      load_row(v + kThreads / 32, na, nb, nd);
+    }
     uint32_t c[8];
     {
       const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
@@ -243,15 +327,57 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
   pdl_trigger();  // the select chain (PDL) may start launching
 }
 
+// Tensor map over the batch as [n][H][3W/8] u64 (row pitch 3W, frame pitch in_fs; both
+// multiples of 16 on this path), box = one 1,536-byte row segment.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+bool make_row_map(const uint8_t* in, int64_t in_fs, int n, int H, int W, CUtensorMap* map) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)(3LL * W / 8), (cuuint64_t)H, (cuuint64_t)n};
+  const cuuint64_t strides[2] = {(cuuint64_t)(3LL * W), (cuuint64_t)in_fs};
+  const cuuint32_t box[3] = {kTmaRowBytes / 8, 1, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint8_t*>(in), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+bool use_tma() {  // read per launch (tests switch it inside one process)
+  const char* e = std::getenv("DHZ_K1_TMA");
+  return e && e[0] == '1';
+}
+
 template <int R>
 cudaError_t launch(const uint8_t* in, int64_t in_fs, int n, int H, int W, uint8_t* dark, int64_t dark_fs,
                    uint32_t* frame_max, uint32_t* unit_max, cudaStream_t st) {
   using G = RowGeo<R>;
-  auto kern = k_dark_rows<R>;
+  dim3 grid((W + kTW - 1) / kTW, (H + kBH - 1) / kBH, n);
+  CUtensorMap map{};
+  // the map's frame pitch must be >= one frame and the innermost extent a whole number of u64
+  if (use_tma() && R <= 8 && (3LL * W) % 8 == 0 && (n == 1 || in_fs >= 3LL * W * H) &&
+      make_row_map(in, n == 1 ? 3LL * W * H : in_fs, n, H, W, &map)) {
+    auto kern = k_dark_rows<R, true>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_TMA);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kThreads, G::SMEM_TMA, st>>>(in, in_fs, H, W, dark, dark_fs, frame_max, unit_max, map);
+    return cudaGetLastError();
+  }
+  auto kern = k_dark_rows<R, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
   if (e != cudaSuccess) return e;
-  dim3 grid((W + kTW - 1) / kTW, (H + kBH - 1) / kBH, n);
-  kern<<<grid, kThreads, G::SMEM, st>>>(in, in_fs, H, W, dark, dark_fs, frame_max, unit_max);
+  kern<<<grid, kThreads, G::SMEM, st>>>(in, in_fs, H, W, dark, dark_fs, frame_max, unit_max, map);
   return cudaGetLastError();
 }
 

@@ -107,3 +107,70 @@ def dehaze_sharded(frames_local: torch.Tensor, params, n_frames: int, stabilise:
         trace = stabilise_trace(trace, float(stabilise))
     out = eng.phase_recover(frames_local, params, trace[lo:hi].contiguous())
     return out, trace
+
+
+class ShardedPipeline:
+    """A fixed (frames_local, params) shard replayed step after step under torch.distributed.
+
+    ``dehaze_sharded`` with its two halves captured once as CUDA graphs (the kernels'
+    launch gaps go; the buffers are fixed) around an eager NCCL all-gather into a
+    preallocated trace — the collective itself is not captured.  ``frames_local`` is
+    updated in place between steps.  ``step()`` returns (out_local, airlight_trace);
+    both are reused by the next step.
+    """
+
+    def __init__(self, frames_local: torch.Tensor, params, n_frames: int, stabilise: float | None = None,
+                 group=None):
+        from .engine import FrameEngine
+
+        params.validate()
+        self.group = group
+        self.stabilise = None if stabilise is None else float(stabilise)
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        sizes = [shard_range(n_frames, r, world) for r in range(world)]
+        self.lo, self.hi = sizes[rank]
+        n = self.hi - self.lo
+        if frames_local.shape[0] != n:
+            raise ValueError(f"rank {rank} holds {frames_local.shape[0]} frames, shard_range gives {n}")
+        dev = frames_local.device
+        cap = max(hi - lo for lo, hi in sizes)
+        self.frames = frames_local
+        self._pad = torch.zeros((cap, 3), dtype=torch.float64, device=dev)   # this rank's block, padded
+        self._air_raw = self._pad[:n]
+        self._gathered = torch.empty((world * cap, 3), dtype=torch.float64, device=dev)
+        self._pick = None
+        if any(hi - lo != cap for lo, hi in sizes):  # uneven blocks: drop the padding rows
+            self._pick = torch.tensor([r * cap + i for r, (lo, hi) in enumerate(sizes) for i in range(hi - lo)],
+                                      dtype=torch.int64, device=dev)
+        self._air_in = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        h, w = int(frames_local.shape[1]), int(frames_local.shape[2])
+        H, W = FrameEngine.working_size(params, h, w)
+        self.out = torch.empty((n, H, W, 3), dtype=torch.uint8, device=dev)
+        self._eng = FrameEngine(dev)  # private engine: the graphs keep its workspace
+        self._g1 = self._g2 = None
+        if n:
+            first = lambda: self._eng.phase_airlight(self.frames, params, airlight=self._air_raw)  # noqa: E731
+            second = lambda: self._eng.phase_recover(self.frames, params, self._air_in, out=self.out)  # noqa: E731
+            first()  # eager warm-up: workspace, thresholds, kernel attributes
+            self._air_in.copy_(self._air_raw)
+            second()
+            torch.cuda.synchronize(dev)
+            self._g1, self._g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self._g1):
+                first()
+            with torch.cuda.graph(self._g2):
+                second()
+            torch.cuda.synchronize(dev)
+
+    def step(self):
+        if self._g1 is not None:
+            self._g1.replay()
+        dist.all_gather_into_tensor(self._gathered, self._pad, group=self.group)
+        trace = self._gathered if self._pick is None else self._gathered.index_select(0, self._pick)
+        if self.stabilise is not None:
+            trace = stabilise_trace(trace, self.stabilise)
+        if self._g2 is not None:
+            self._air_in.copy_(trace[self.lo:self.hi])
+            self._g2.replay()
+        return self.out, trace

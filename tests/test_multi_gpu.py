@@ -180,5 +180,17 @@ def test_dehaze_sharded_world1_nccl():
         out, trace = dehaze_sharded(f, p, 6, stabilise=0.9)
         w2, a2 = dehaze_batch(f, p, stabilise=0.9)
         assert torch.equal(out, w2) and torch.equal(trace, a2)
+        # the graph-replayed form of the same step (bench.py --gpus N): frames updated in place
+        from paper_2512_16609_b200.distributed import ShardedPipeline
+
+        for params, kw in ((p, {}), (p, {"stabilise": 0.9}), (DehazeParams(), {}),
+                           (DehazeParams(mode="image", resize_to=None, guided_radius=6), {})):
+            g = f.clone()
+            pipe = ShardedPipeline(g, params, 6, **kw)
+            for frames in (f, f.flip(0).contiguous()):
+                g.copy_(frames)
+                out, trace = pipe.step()
+                want, wair = dehaze_batch(frames, params, **kw)
+                assert torch.equal(out, want) and torch.equal(trace, wair)
     finally:
         dist.destroy_process_group()

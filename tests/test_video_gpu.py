@@ -176,6 +176,33 @@ def test_k1_tiles_every_radius(oracle, r):
     _check(np.stack([f0, f1, f2]), _params(patch_radius=r), oracle)
 
 
+@pytest.mark.parametrize("r", [1, 4, 7, 8])
+def test_k1_tma_variant(oracle, r, monkeypatch):
+    """DHZ_K1_TMA=1: K1 with its rows staged by cp.async.bulk.tensor (one stage and one
+    mbarrier per warp) instead of LDG.128: same geometry cases as the tile test (partial
+    tiles on both axes, so rows and columns outside the frame arrive as TMA zero fill and
+    must read as the all-ones neutral), against the oracle and bit-identical to the default."""
+    rng = np.random.default_rng(900 + r)
+    H, W = 130, 976
+    f0 = rng.integers(0, 256, size=(H, W, 3), dtype=np.uint8)
+    f1 = np.full((H, W, 3), 200, dtype=np.uint8)
+    f1[::7, ::11] = 0
+    f1[:3] = 255
+    f1[-2:, -20:] = 1
+    frames = np.stack([f0, f1])
+    base = _run(frames, _params(patch_radius=r))
+    monkeypatch.setenv("DHZ_K1_TMA", "1")
+    tma = _run(frames, _params(patch_radius=r))
+    for a, b in zip(base, tma):
+        assert np.array_equal(a, b)
+    _check(frames, _params(patch_radius=r), oracle)
+    one = _run(frames[:1, :40, :32], _params(patch_radius=r))  # a single small frame (frame pitch = its size)
+    monkeypatch.delenv("DHZ_K1_TMA")
+    ref = _run(frames[:1, :40, :32], _params(patch_radius=r))
+    for a, b in zip(ref, one):
+        assert np.array_equal(a, b)
+
+
 def test_balance_out_of_band_samples(oracle):
     # uniform noise: most non-minimum samples lie >= 64 levels above their pixel's
     # minimum, outside the banded table (k_balance_band's per-unit correction path)
