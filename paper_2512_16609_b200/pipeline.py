@@ -530,6 +530,29 @@ def _par_copy(dst, src):
 _STREAM_BATCH_MAX = 256
 _PIPE_BATCH_BYTES = 48 << 20      # native path: input bytes per pipelined batch
 _PIPE_SLOTS = 3
+# Fresh output frames are handed out as numpy views of their own pinned host tensors (the
+# D2H copy lands in them directly: no staging copy, no first-touch page faults) while the
+# bytes still held by the caller stay under this budget; past it (a sink that keeps every
+# frame of a long clip) outputs are copied out of the slot's staging into plain arrays.
+_PINNED_OUT_BUDGET = int(__import__("os").environ.get("DHZ_PINNED_OUT_BYTES", 1 << 30))
+_PINNED_OUT_MIN = 1 << 20   # smaller frames (VGA): the staging copy is cheaper than a pinned tensor each
+_pinned_out_lock = __import__("threading").Lock()
+_pinned_out_bytes = 0
+
+
+def _pinned_out_take(nbytes):
+    global _pinned_out_bytes
+    with _pinned_out_lock:
+        if _pinned_out_bytes + nbytes > _PINNED_OUT_BUDGET:
+            return False
+        _pinned_out_bytes += nbytes
+        return True
+
+
+def _pinned_out_release(nbytes):
+    global _pinned_out_bytes
+    with _pinned_out_lock:
+        _pinned_out_bytes -= nbytes
 
 
 class _StreamPipe:
@@ -579,6 +602,10 @@ class _StreamPipe:
         self.prev = None  # (slot, rows) of the last submitted batch (stabilise carry source)
         self.fresh = fresh  # False: emit views of the pinned output (the consumer copies at once)
         self._emit = None
+        self._pending = None       # (slot, rows, copy futures) of a closed batch not launched yet
+        self.own = [None] * S      # per slot: the batch's own pinned output tensors (fresh mode)
+        self.lazy = [[] for _ in range(S)]  # per slot: (row, frame) copies deferred to submit()
+        self.out_bytes = OH * OW * 3
 
     def next_input(self, emit=None):
         """The pinned input frame the next frame goes into (drains the slot's previous batch first)."""
@@ -593,18 +620,61 @@ class _StreamPipe:
         if self.fill == self.batch:
             self.submit()
 
-    def put(self, frame, emit):
+    def put(self, frame, emit, persistent=False):
+        """Stage one frame.  ``persistent``: the caller keeps ``frame`` alive and unchanged
+        until the stream ends (a list of frames), so its copy into the pinned slot may wait
+        for submit(), where the batch's copies run side by side on the copy threads;
+        otherwise the copy is done before returning (the source may reuse its buffer)."""
         import torch
 
-        _par_copy(self.next_input(emit), torch.from_numpy(frame))  # done before the source reuses its buffer
+        dst = self.next_input(emit)
+        if persistent and frame.nbytes >= (1 << 19):
+            self.lazy[self.slot].append((dst, frame))
+        else:
+            _par_copy(dst, torch.from_numpy(frame))
         self.commit(emit)
 
     def submit(self):
+        """Close the slot being filled.  Its deferred staging copies start on the copy
+        threads and the ring moves on at once; the batch is launched (H2D, pipeline, D2H)
+        at the next submit()/finish(), after the previously closed batch's copies — so
+        the host copies of batch k+1 run while batch k is being enqueued."""
         import torch
 
         s, m = self.slot, self.fill
         if m == 0:
+            self._launch_pending()
             return
+        lazy, futs = self.lazy[s], None
+        if lazy:
+            if len(lazy) > 1:
+                futs = [_pool().submit(job[0].copy_, torch.from_numpy(job[1])) for job in lazy]
+            else:
+                _par_copy(lazy[0][0], torch.from_numpy(lazy[0][1]))
+            lazy.clear()
+        self.slot = (s + 1) % len(self.hin)
+        self.fill = 0
+        self._launch_pending()
+        if futs is None:
+            self._launch(s, m)
+        else:
+            self._pending = (s, m, futs)
+
+    def _launch_pending(self):
+        if self._pending is not None:
+            s, m, futs = self._pending
+            self._pending = None
+            for f in futs:
+                f.result()
+            self._launch(s, m)
+
+    def _launch(self, s, m):
+        import torch
+
+        own = None
+        if self.fresh and self.out_bytes >= _PINNED_OUT_MIN and _pinned_out_take(m * self.out_bytes):
+            own = [torch.empty(self.out_shape, dtype=torch.uint8, pin_memory=True) for _ in range(m)]
+        self.own[s] = own
         st = self.streams[s]
         with torch.cuda.stream(st):
             self.din[s][:m].copy_(self.hin[s][:m], non_blocking=True)
@@ -616,13 +686,15 @@ class _StreamPipe:
                 carry = self.carry[s]
             self.engines[s].run(self.din[s][:m], self.params, out=self.dout[s][:m], airlight=self.dair[s][:m],
                                 stream=st, stabilise=self.lam, carry=carry)
-            self.hout[s][:m].copy_(self.dout[s][:m], non_blocking=True)
+            if own is not None:
+                for i in range(m):
+                    own[i].copy_(self.dout[s][i], non_blocking=True)
+            else:
+                self.hout[s][:m].copy_(self.dout[s][:m], non_blocking=True)
             self.hair[s][:m].copy_(self.dair[s][:m], non_blocking=True)
             self.events[s].record(st)
         self.inflight[s] = m
         self.prev = (s, m)
-        self.slot = (s + 1) % len(self.hin)
-        self.fill = 0
 
     def drain(self, s, emit):
         import torch
@@ -631,7 +703,15 @@ class _StreamPipe:
         if not m:
             return
         self.events[s].synchronize()
-        if self.fresh:  # the sink may keep them: fresh arrays, filled by the copy threads
+        own, self.own[s] = self.own[s], None
+        if own is not None:  # each frame owns its pinned tensor; the budget follows the arrays' lifetime
+            import weakref
+
+            outs = [t.numpy() for t in own]
+            for o in outs:
+                weakref.finalize(o, _pinned_out_release, self.out_bytes)
+            del own
+        elif self.fresh:  # the sink may keep them: fresh arrays, filled by the copy threads
             outs = [np.empty(self.out_shape, dtype=np.uint8) for _ in range(m)]
             hout = self.hout[s]
             if m > 1 and outs[0].nbytes >= (1 << 19):
@@ -645,8 +725,18 @@ class _StreamPipe:
             emit(outs[i], self.hair[s][i].numpy().copy())
         self.inflight[s] = 0
 
+    def __del__(self):  # a stream abandoned mid-way (the sink raised): return its share of the budget
+        try:
+            for s, own in enumerate(self.own):
+                if own is not None:
+                    _pinned_out_release(len(own) * self.out_bytes)
+                    self.own[s] = None
+        except Exception:
+            pass
+
     def finish(self, emit):
         self.submit()
+        self._launch_pending()
         S = len(self.hin)
         for k in range(S):  # oldest first: the slot after the last submitted one
             self.drain((self.slot + k) % S, emit)
@@ -679,6 +769,9 @@ def process_stream(frames, params=None, sink=None, workers=1, devices=None, stab
         n_hint = len(frames)
     except TypeError:
         n_hint = None
+    # a list's frames stay alive and unchanged for the whole call: their staging copies may be
+    # deferred and run in parallel (an iterator may reuse its buffer, so it is copied at once)
+    persistent = isinstance(frames, (list, tuple)) and __import__("os").environ.get("DHZ_PS_LAZY", "1") != "0"
     trace = []
     count = 0
     expected_shape = None
@@ -743,7 +836,7 @@ def process_stream(frames, params=None, sink=None, workers=1, devices=None, stab
             flush()
             raise
         if pipe is not None:
-            pipe.put(frame, emit)
+            pipe.put(frame, emit, persistent=persistent)
             continue
         pending.append(frame)
         if len(pending) >= limit:

@@ -233,6 +233,43 @@ class TestPipeline:
         empty = dz.process_stream([], p)
         assert empty.frame_count == 0 and empty.airlight_trace == []
 
+    def test_stream_outputs_own_their_memory(self, dz, monkeypatch):
+        """Fresh outputs are views of their own pinned tensors while the caller-held bytes
+        fit the budget, plain arrays past it; the bytes are the same either way, kept
+        frames stay intact while later batches run, and dropped frames return the budget."""
+        import gc
+
+        from paper_2512_16609_b200 import pipeline as pl
+        from paper_2512_16609_b200.synthetic import make_frames
+
+        frames = list(make_frames("c3", frames=40, width=800, height=448).numpy())  # >= 1 MiB each: own pinned outputs
+        p = dz.DehazeParams(resize_to=None)
+        monkeypatch.setattr(pl, "_PIPE_BATCH_BYTES", 4 * frames[0].nbytes)  # 4 frames per batch: slots get reused
+        gc.collect()
+        base = pl._pinned_out_bytes
+        kept = []
+        dz.process_stream(frames, p, sink=kept.append)
+        assert pl._pinned_out_bytes == base + 40 * frames[0].nbytes
+        snap = [k.copy() for k in kept]
+        again = []
+        dz.process_stream(iter(frames), p, sink=again.append)   # iterator: immediate copies
+        assert all(np.array_equal(a, b) for a, b in zip(kept, snap))
+        assert all(np.array_equal(a, b) for a, b in zip(kept, again))
+        monkeypatch.setattr(pl, "_PINNED_OUT_BUDGET", 0)        # past the budget: copied out of staging
+        plain = []
+        dz.process_stream(frames, p, sink=plain.append)
+        assert all(np.array_equal(a, b) for a, b in zip(kept, plain))
+        assert all(o.flags.owndata for o in plain) and not any(o.flags.owndata for o in kept)
+        want = dz.dehaze_frame(frames[17], p)
+        assert np.array_equal(kept[17], want)
+        view = kept[3][5:9]
+        del kept, again
+        gc.collect()
+        assert pl._pinned_out_bytes == base + frames[0].nbytes   # the view keeps its frame's buffer
+        del view
+        gc.collect()
+        assert pl._pinned_out_bytes == base
+
     def test_batch_and_host_batch_match_frame_api(self, dz):
         import torch
 
