@@ -555,6 +555,32 @@ def _pinned_out_release(nbytes):
         _pinned_out_bytes -= nbytes
 
 
+_pipe_cache = __import__("threading").local()   # .entry = (key, pipe): the calling thread's last pipe
+
+
+def _acquire_pipe(devs, params, shape, stabilise, n_hint):
+    """process_stream's pipe: the thread's previous one when the geometry is the same
+    (staging, device buffers, streams and engines are reused: a one-frame stream costs no
+    set-up), a new one otherwise or when that one is busy (a sink calling process_stream)."""
+    probe_batch = max(1, min(_STREAM_BATCH_MAX, _PIPE_BATCH_BYTES // (3 * shape[0] * shape[1])))
+    if n_hint is not None:
+        probe_batch = max(1, min(probe_batch, -(-int(n_hint) // _PIPE_SLOTS)))
+    from .engine import FrameEngine
+
+    key = (tuple((d.type, d.index) for d in devs), tuple(shape), FrameEngine.working_size(params, shape[0], shape[1]),
+           probe_batch)
+    entry = getattr(_pipe_cache, "entry", None)
+    if entry is not None and entry[0] == key and not entry[1].busy:
+        pipe = entry[1]
+        pipe.reset(params, stabilise)
+    else:
+        pipe = _StreamPipe(devs, params, shape, stabilise=stabilise, n_hint=n_hint)
+        if entry is None or not entry[1].busy:
+            _pipe_cache.entry = (key, pipe)
+    pipe.busy = True
+    return pipe
+
+
 class _StreamPipe:
     """process_stream's pipelined batches on the native path.
 
@@ -603,9 +629,30 @@ class _StreamPipe:
         self.fresh = fresh  # False: emit views of the pinned output (the consumer copies at once)
         self._emit = None
         self._pending = None       # (slot, rows, copy futures) of a closed batch not launched yet
+        self.busy = False          # held by a running process_stream (see _acquire_pipe)
         self.own = [None] * S      # per slot: the batch's own pinned output tensors (fresh mode)
         self.lazy = [[] for _ in range(S)]  # per slot: (row, frame) copies deferred to submit()
         self.out_bytes = OH * OW * 3
+
+    def reset(self, params, stabilise):
+        """Ready a cached pipe for another stream: wait for anything an aborted stream left
+        in flight, return its share of the pinned-output budget, clear the ring."""
+        for f in (self._pending[2] if self._pending is not None else ()):
+            try:
+                f.result()
+            except Exception:
+                pass
+        for s, m in enumerate(self.inflight):
+            if m:
+                self.events[s].synchronize()
+            if self.own[s] is not None:
+                _pinned_out_release(len(self.own[s]) * self.out_bytes)
+                self.own[s] = None
+            self.inflight[s] = 0
+            self.lazy[s].clear()
+        self.params, self.lam = params, stabilise
+        self.slot = self.fill = 0
+        self.prev = self._pending = self._emit = None
 
     def next_input(self, emit=None):
         """The pinned input frame the next frame goes into (drains the slot's previous batch first)."""
@@ -801,47 +848,50 @@ def process_stream(frames, params=None, sink=None, workers=1, devices=None, stab
             emit(out_h[i], air_h[i].copy())
         pending.clear()
 
-    it = iter(frames)
-    index = -1
-    while True:
-        index += 1
-        try:
-            frame = next(it)
-        except StopIteration:
-            break
-        except BaseException:
-            flush()  # frames before a failing source (e.g. a truncated stream) still reach the sink
-            raise
-        try:
-            frame = check_u8_frame(frame, name=f"frame {index}")
-            if not isinstance(frame, np.ndarray):
-                frame = frame.cpu().numpy()
-            if expected_shape is None:
-                expected_shape = frame.shape
-                dev = _device()
-                per = frame.nbytes
-                limit = max(1, min(_STREAM_BATCH_MAX, _STREAM_BATCH_BYTES // max(per, 1)))
-                if _native_ok(params, frame.shape[0], frame.shape[1]):
-                    pipe = _StreamPipe(devs if devs is not None else [dev], params, frame.shape, stabilise=lam,
-                                       n_hint=n_hint)
-                elif devs is not None or lam is not None:
-                    raise ValueError("devices= / stabilise= need a call the batched native pipeline covers "
-                                     "(see _native_ok)")
-            elif frame.shape != expected_shape:
-                raise ValueError(
-                    f"frame {index} has size {frame.shape[1]}x{frame.shape[0]}, "
-                    f"expected {expected_shape[1]}x{expected_shape[0]}"
-                )
-        except ValueError:
-            flush()
-            raise
+    try:
+        it = iter(frames)
+        index = -1
+        while True:
+            index += 1
+            try:
+                frame = next(it)
+            except StopIteration:
+                break
+            except BaseException:
+                flush()  # frames before a failing source (e.g. a truncated stream) still reach the sink
+                raise
+            try:
+                frame = check_u8_frame(frame, name=f"frame {index}")
+                if not isinstance(frame, np.ndarray):
+                    frame = frame.cpu().numpy()
+                if expected_shape is None:
+                    expected_shape = frame.shape
+                    dev = _device()
+                    per = frame.nbytes
+                    limit = max(1, min(_STREAM_BATCH_MAX, _STREAM_BATCH_BYTES // max(per, 1)))
+                    if _native_ok(params, frame.shape[0], frame.shape[1]):
+                        pipe = _acquire_pipe(devs if devs is not None else [dev], params, frame.shape, lam, n_hint)
+                    elif devs is not None or lam is not None:
+                        raise ValueError("devices= / stabilise= need a call the batched native pipeline covers "
+                                         "(see _native_ok)")
+                elif frame.shape != expected_shape:
+                    raise ValueError(
+                        f"frame {index} has size {frame.shape[1]}x{frame.shape[0]}, "
+                        f"expected {expected_shape[1]}x{expected_shape[0]}"
+                    )
+            except ValueError:
+                flush()
+                raise
+            if pipe is not None:
+                pipe.put(frame, emit, persistent=persistent)
+                continue
+            pending.append(frame)
+            if len(pending) >= limit:
+                flush()
+        flush()
+    finally:
         if pipe is not None:
-            pipe.put(frame, emit, persistent=persistent)
-            continue
-        pending.append(frame)
-        if len(pending) >= limit:
-            flush()
-    flush()
+            pipe.busy = False  # back to the thread's cache (see _acquire_pipe)
 
     wall = time.perf_counter() - start
     fps = count / wall if wall > 0 and count else 0.0
