@@ -64,17 +64,20 @@ __device__ __forceinline__ void tma_load_row(void* dst, const CUtensorMap* map, 
 }
 
 constexpr int kTW = kBandW;  // output columns per tile (30 lanes x 16 px)
-constexpr int kBH = 64;    // output rows per tile
+constexpr int kBH = 64;    // output rows per tile (large batches)
+constexpr int kBHSmall = 16;  // small batches (a frame or two): 4x the CTAs, each a quarter of the
+                              // serial work — the halo rows it re-reads come from L2 and the
+                              // launch is latency-bound anyway (one VGA frame: 16 -> 60 CTAs)
 constexpr int kRun = kBandH;  // rows per pass-2 item (== unit height of unit_max)
 constexpr int kThreads = 256;
 #ifndef DHZ_K1_MINB
 #define DHZ_K1_MINB 4  // resident CTAs per SM the register budget is sized for
 #endif
 
-template <int R>
+template <int R, int BH = kBH>
 struct RowGeo {
   static constexpr int L = 2 * R + 1;
-  static constexpr int ROWS = kBH + 2 * R;
+  static constexpr int ROWS = BH + 2 * R;
   static constexpr int P = L >= 27 ? 27 : (L >= 9 ? 9 : (L >= 3 ? 3 : 1));
   static constexpr int HPR = (R + 1) / 2;        // neighbour pairs borrowed each side
   static constexpr int NP = 2 * HPR + 8 + 1;     // local pairs (+1 neutral pad)
@@ -135,16 +138,16 @@ __device__ __forceinline__ uint32_t vert_final(const uint32_t (&v)[N], int j) {
   return min3(v[j], v[j + P], v[j + L - P]);
 }
 
-template <int R, bool TMA>
+template <int R, bool TMA, int BH>
 __global__ void __launch_bounds__(kThreads, R <= 8 ? DHZ_K1_MINB : 1)
 k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t* __restrict__ dark,
             int64_t dark_fs, uint32_t* __restrict__ frame_max, uint32_t* __restrict__ unit_max,
             const __grid_constant__ CUtensorMap tmap) {
-  using G = RowGeo<R>;
+  using G = RowGeo<R, BH>;
   constexpr int L = G::L, P = G::P, HPR = G::HPR, NP = G::NP;
   extern __shared__ __align__(128) uint8_t hrow[];  // [ROWS][kTW] horizontal minima (+ TMA stages)
   const int f = blockIdx.z;
-  const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kBH;
+  const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * BH;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint8_t* frame = in + (int64_t)f * in_fs;
 
@@ -261,13 +264,12 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
 
   // ---------------- pass 2: vertical min, thread per 4 columns x 16 rows ----------------
   constexpr int NG = kTW / 4;                 // 120 column groups
-  // the warp shuffles below need whole warps in every iteration of the item loop
-  static_assert((NG * (kBH / kRun)) % 32 == 0, "pass-2 items must fill whole warps");
+  static_assert(BH % kRun == 0, "tiles hold whole runs");
   static_assert(NG % 8 == 0 && kTW % kUnitW == 0 && kRun == kBandH, "unit maxima: 8 groups of 4 columns");
-  static_assert(((kTW / kUnitW) * (kBH / kRun) + 31) / 32 * 32 <= kThreads, "one thread per unit");
+  static_assert(((kTW / kUnitW) * (BH / kRun) + 31) / 32 * 32 <= kThreads, "one thread per unit");
   constexpr int N = kRun + 2 * R;
-  __shared__ __align__(16) uint32_t item_max[NG * (kBH / kRun)];
-  for (int it = threadIdx.x; it < NG * (kBH / kRun); it += kThreads) {
+  __shared__ __align__(16) uint32_t item_max[NG * (BH / kRun)];
+  for (int it = threadIdx.x; it < NG * (BH / kRun); it += kThreads) {
     const int run = it / NG, g = it - run * NG;
     const int j0 = run * kRun;
     const int xo = x0 + 4 * g;
@@ -307,7 +309,7 @@ k_dark_rows(const uint8_t* __restrict__ in, int64_t in_fs, int H, int W, uint8_t
   __syncthreads();
   // unit maxima (8 column groups of 4 = 32 columns) and the frame maximum
   constexpr int NU = kTW / kUnitW;  // 15 units per tile row
-  constexpr int NUT = NU * (kBH / kRun);
+  constexpr int NUT = NU * (BH / kRun);
   if (threadIdx.x < (NUT + 31) / 32 * 32) {  // whole warps: the shuffles below need them
     uint32_t um = 0;
     if (threadIdx.x < NUT) {
@@ -359,22 +361,37 @@ bool use_tma() {  // read per launch (tests switch it inside one process)
   return e && e[0] == '1';
 }
 
+bool small_tiles(int n, int H, int W) {  // fewer 64-row tiles than two per SM: cut them in four
+  if (const char* e = std::getenv("DHZ_K1_BH")) return std::atoi(e) == kBHSmall;  // tests force either
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return (int64_t)n * ((W + kTW - 1) / kTW) * ((H + kBH - 1) / kBH) < 2LL * sms;
+}
+
 template <int R>
 cudaError_t launch(const uint8_t* in, int64_t in_fs, int n, int H, int W, uint8_t* dark, int64_t dark_fs,
                    uint32_t* frame_max, uint32_t* unit_max, cudaStream_t st) {
   using G = RowGeo<R>;
-  dim3 grid((W + kTW - 1) / kTW, (H + kBH - 1) / kBH, n);
   CUtensorMap map{};
+  if (small_tiles(n, H, W)) {
+    using GS = RowGeo<R, kBHSmall>;
+    dim3 grid((W + kTW - 1) / kTW, (H + kBHSmall - 1) / kBHSmall, n);
+    k_dark_rows<R, false, kBHSmall><<<grid, kThreads, GS::SMEM, st>>>(in, in_fs, H, W, dark, dark_fs, frame_max,
+                                                                      unit_max, map);
+    return cudaGetLastError();
+  }
+  dim3 grid((W + kTW - 1) / kTW, (H + kBH - 1) / kBH, n);
   // the map's frame pitch must be >= one frame and the innermost extent a whole number of u64
   if (use_tma() && R <= 8 && (3LL * W) % 8 == 0 && (n == 1 || in_fs >= 3LL * W * H) &&
       make_row_map(in, n == 1 ? 3LL * W * H : in_fs, n, H, W, &map)) {
-    auto kern = k_dark_rows<R, true>;
+    auto kern = k_dark_rows<R, true, kBH>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_TMA);
     if (e != cudaSuccess) return e;
     kern<<<grid, kThreads, G::SMEM_TMA, st>>>(in, in_fs, H, W, dark, dark_fs, frame_max, unit_max, map);
     return cudaGetLastError();
   }
-  auto kern = k_dark_rows<R, false>;
+  auto kern = k_dark_rows<R, false, kBH>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
   if (e != cudaSuccess) return e;
   kern<<<grid, kThreads, G::SMEM, st>>>(in, in_fs, H, W, dark, dark_fs, frame_max, unit_max, map);

@@ -158,12 +158,17 @@ def test_batches_beyond_the_grid_limit(oracle):
         assert np.array_equal(out[i], want) and np.array_equal(air[i], m["airlight"])
 
 
+@pytest.mark.parametrize("bh,direct", [(64, "0"), (16, "1")])
 @pytest.mark.parametrize("r", list(range(1, 17)))
-def test_k1_tiles_every_radius(oracle, r):
+def test_k1_tiles_every_radius(oracle, r, bh, direct, monkeypatch):
     """K1's vectorised path (width % 16 == 0, r <= 16) across tile seams: 130 rows
     (three 64-row tile rows, the last partial), 976 columns (three 480-column tiles,
     the last partial); plateaus, extreme values and noise so every lane of the
-    16-bit pairs sees 0, 255 and ties."""
+    16-bit pairs sees 0, 255 and ties.  Both tile heights (64 rows: large batches;
+    16 rows: the small-batch launch, nine tile rows here) and both K6 forms (table in
+    shared memory; direct gathers for small batches) are forced in turn."""
+    monkeypatch.setenv("DHZ_K1_BH", str(bh))
+    monkeypatch.setenv("DHZ_K6_DIRECT", direct)
     rng = np.random.default_rng(500 + r)
     H, W = 130, 976
     f0 = rng.integers(0, 256, size=(H, W, 3), dtype=np.uint8)
