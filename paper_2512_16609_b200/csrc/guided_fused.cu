@@ -36,6 +36,7 @@
 // virtual rows the edge rows' a, b (kept per thread in a small global scratch).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include "dhz_common.cuh"
@@ -66,6 +67,7 @@ struct FusedArgs {
   double inv_gamma;
   int gamma_is_one;
   int pow_general;         // 1: pow_tab (inv_gamma outside the series' range)
+  int gw_bf;               // k_gw_sums: branch-free series terms (DHZ_GW_BF=0 turns them off for A/B)
   double h[9];             // binomial series coefficients C(inv_gamma, k), k = 1..8
   uint8_t* out;
   int64_t out_fs;
@@ -136,6 +138,29 @@ __device__ __forceinline__ unsigned long long gw_term(double f255v, double Ac, d
                                                       const SeriesTables& PT) {
   const double x = fmin(fmax(__fma_rn(__dsub_rn(f255v, Ac), rt, Ac), 0.0), 1.0);
   const double g = A.gamma_is_one ? x : (A.pow_general ? pow_general_ool(x, A.inv_gamma) : pow_series(x, A, PT));
+  return (unsigned long long)__double_as_longlong(__fma_rn(g, 0x1p38, 0x1.8p52));
+}
+
+// gw_term without branches, for the streaming sums kernel (series path only: gamma != 1,
+// inv_gamma <= 16).  Same operations on the same inputs as gw_term / pow_series, with the
+// x <= 0 and x >= 1 exits as selects; a sample in (0, 2^-64) — pow_series hands those to
+// the general pow — sets `rare`, and the caller redoes its group with gw_term.
+__device__ __forceinline__ unsigned long long gw_term_bf(double f255v, double Ac, double rt, const FusedArgs& A,
+                                                         const SeriesTables& S, bool& rare) {
+  const double x = fmin(fmax(__fma_rn(__dsub_rn(f255v, Ac), rt, Ac), 0.0), 1.0);
+  rare |= (x > 0.0) & (x < 0x1p-64);
+  const long long bits = __double_as_longlong(fmax(x, 0x1p-64));  // k in [0, 64]
+  const int k = 1023 - (int)(bits >> 52);
+  const int j = (int)((bits >> 42) & 1023);
+  const double m = __longlong_as_double((bits & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
+  const double u = __fma_rn(m, S.ri[j], -1.0);
+  double s = A.h[4];
+#pragma unroll
+  for (int i = 3; i >= 1; --i) s = __fma_rn(s, u, A.h[i]);
+  const double pm = __fma_rn(s, u, 1.0);
+  double g = __dmul_rn(__dmul_rn(S.ce[j], pm), S.p2[k]);
+  g = x >= 1.0 ? 1.0 : g;
+  g = x >= 0x1p-64 ? g : 0.0;
   return (unsigned long long)__double_as_longlong(__fma_rn(g, 0x1p38, 0x1.8p52));
 }
 
@@ -1394,12 +1419,33 @@ __global__ void __launch_bounds__(kXThreads, 2) k_gx_out(FusedArgs A, int nframe
   }
 }
 
+// A 4-pixel group's gray-world terms by the general gw_term (any gamma, partial groups,
+// samples below 2^-64), out of line: the streaming loop below keeps its registers for
+// the branch-free series path.
+__device__ __noinline__ void gw_group_general(uint32_t w0, uint32_t w1, uint32_t w2, double t0, double t1, double t2,
+                                              double t3, int np, double A0, double A1, double A2, const FusedArgs& A,
+                                              const SeriesTables& PT, const double* s_f, unsigned long long& b0,
+                                              unsigned long long& b1, unsigned long long& b2) {
+  const uint32_t w[3] = {w0, w1, w2};
+  const double t[4] = {t0, t1, t2, t3};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (u >= np) break;
+    uint32_t R, Gc, B;
+    rgb_of(w, u, R, Gc, B);
+    const double rt = __drcp_rn(t[u]);
+    b0 += gw_term(s_f[R], A0, rt, A, PT) - kGwBias;
+    b1 += gw_term(s_f[Gc], A1, rt, A, PT) - kGwBias;
+    b2 += gw_term(s_f[B], A2, rt, A, PT) - kGwBias;
+  }
+}
+
 // Gray-world channel sums of the two-pass form, a streaming pass over t~ and the frame:
 // per pixel the three gw_term values (the same function as the one-pass kernel's
 // inline sums, exact integer totals, so the same per-frame sums), kept out of the
 // box-filter kernel whose register file and shared memory they would share.
 // Persistent CTAs over the batch's 4-pixel groups, per-frame u64 totals by atomics.
-__global__ void __launch_bounds__(256) k_gw_sums(FusedArgs A, int n, int64_t npx) {
+__global__ void __launch_bounds__(256, 4) k_gw_sums(const __grid_constant__ FusedArgs A, int n, int64_t npx) {
   __shared__ SeriesTables PT;
   __shared__ double s_f[256];
   for (int v = threadIdx.x; v < 256; v += blockDim.x) s_f[v] = __ddiv_rn((double)v, 255.0);
@@ -1410,6 +1456,7 @@ __global__ void __launch_bounds__(256) k_gw_sums(FusedArgs A, int n, int64_t npx
   const int64_t g0 = total * blockIdx.x / gridDim.x, g1 = total * (blockIdx.x + 1) / gridDim.x;
   const bool vec = (npx & 3) == 0 && (A.in_fs & 3) == 0 && ((uintptr_t)A.in & 3) == 0 &&
                    ((uintptr_t)A.t_out & 15) == 0;
+  const bool series = !A.gamma_is_one && !A.pow_general && A.gw_bf;
   for (int64_t s0 = g0; s0 < g1;) {
     const int f = (int)(s0 / G);
     const int64_t s1 = min(g1, (int64_t)(f + 1) * G);
@@ -1441,16 +1488,26 @@ __global__ void __launch_bounds__(256) k_gw_sums(FusedArgs A, int n, int64_t npx
 #pragma unroll
         for (int q = 0; q < 3; ++q) w[q] = bb[4 * q] | (bb[4 * q + 1] << 8) | (bb[4 * q + 2] << 16) | (bb[4 * q + 3] << 24);
       }
+      if (series && np == 4) {  // whole group on the branch-free series path
+        unsigned long long c0 = 0, c1 = 0, c2 = 0;
+        bool rare = false;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (u >= np) break;
-        uint32_t R, Gc, B;
-        rgb_of(w, u, R, Gc, B);
-        const double rt = __drcp_rn(t[u]);
-        b0 += gw_term(s_f[R], A0, rt, A, PT) - kGwBias;
-        b1 += gw_term(s_f[Gc], A1, rt, A, PT) - kGwBias;
-        b2 += gw_term(s_f[B], A2, rt, A, PT) - kGwBias;
+        for (int u = 0; u < 4; ++u) {
+          uint32_t R, Gc, B;
+          rgb_of(w, u, R, Gc, B);
+          const double rt = __drcp_rn(t[u]);
+          c0 += gw_term_bf(s_f[R], A0, rt, A, PT, rare) - kGwBias;
+          c1 += gw_term_bf(s_f[Gc], A1, rt, A, PT, rare) - kGwBias;
+          c2 += gw_term_bf(s_f[B], A2, rt, A, PT, rare) - kGwBias;
+        }
+        if (!rare) {
+          b0 += c0;
+          b1 += c1;
+          b2 += c2;
+          continue;
+        }
       }
+      gw_group_general(w[0], w[1], w[2], t[0], t[1], t[2], t[3], np, A0, A1, A2, A, PT, s_f, b0, b1, b2);
     }
     unsigned long long v[3] = {b0, b1, b2};
 #pragma unroll
@@ -1635,6 +1692,10 @@ static void x_args(FusedArgs& A, int H, int W, int r, double eps, int64_t in_fs,
   A.inv_gamma = 1.0 / gamma;
   A.gamma_is_one = gamma == 1.0 ? 1 : 0;
   A.pow_general = (A.inv_gamma > 16.0) ? 1 : 0;
+  {
+    const char* e = std::getenv("DHZ_GW_BF");
+    A.gw_bf = (e && e[0] == '0') ? 0 : 1;
+  }
   double c = 1.0;
   A.h[0] = 1.0;
   for (int k = 1; k <= 8; ++k) {
