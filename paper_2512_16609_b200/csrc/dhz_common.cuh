@@ -253,9 +253,14 @@ __device__ __forceinline__ double pow_tab(double x, double e, const PowTables& T
 // none: its byte windows are wider than 1/1024) goes to the caller's exact fp64 path.
 constexpr int kByteBuckets = 1024;
 constexpr double kByteMargin = 1e-6;
+// One 16-byte entry per bucket (a single shared-memory load per sample): the lower window
+// (lo(k0), hi(k0)), the upper window's end hi(k0 + 1) and k0 itself; the upper window's
+// start is formed at lookup time as hi(k0) + kByteGap, which is never below lo(k0 + 1):
+// hi(k0) >= thr - margin - ulp and the float sum rounds by at most another ulp (ulp <=
+// 6e-8 below 1), so hi(k0) + 2.2e-6 >= thr + margin + 8e-8.
+constexpr float kByteGap = 2.2e-6f;
 struct ByteBuckets {
-  float4 ent[kByteBuckets + 1];  // (lo(k0), hi(k0), lo(k0 + 1), hi(k0 + 1))
-  uint8_t k0[kByteBuckets + 8];
+  float4 ent[kByteBuckets + 1];  // (lo(k0), hi(k0), hi(k0 + 1), bits: k0)
 };
 
 // Block-cooperative build from thr[0..255] (thr[0] unused; +inf = unreachable level);
@@ -273,8 +278,7 @@ __device__ __forceinline__ void byte_buckets_build(ByteBuckets& B, const double*
       if (thr[mid] <= x) lo = mid;
       else hi = mid - 1;
     }
-    B.k0[j] = (uint8_t)lo;
-    B.ent[j] = make_float4(lo_of(lo), hi_of(lo), lo_of(lo + 1), hi_of(lo + 1));
+    B.ent[j] = make_float4(lo_of(lo), hi_of(lo), hi_of(lo + 1), __uint_as_float((uint32_t)lo));
   }
 }
 
@@ -282,8 +286,8 @@ __device__ __forceinline__ void byte_buckets_build(ByteBuckets& B, const double*
 __device__ __forceinline__ uint32_t byte_bucket(const ByteBuckets& B, float xf, bool& ok) {
   const uint32_t j = min(__float2uint_rd(xf * (float)kByteBuckets), (uint32_t)kByteBuckets);  // (negative -> 0)
   const float4 e = B.ent[j];
-  const uint32_t k = B.k0[j];
-  const bool in0 = xf >= e.x && xf < e.y, in1 = xf >= e.z && xf < e.w;
+  const uint32_t k = __float_as_uint(e.w);
+  const bool in0 = xf >= e.x && xf < e.y, in1 = xf >= e.y + kByteGap && xf < e.z;
   ok = ok && (in0 || in1);
   return k + (in1 ? 1u : 0u);
 }
