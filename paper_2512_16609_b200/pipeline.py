@@ -272,6 +272,37 @@ def _run_native(batch, params, telemetry=None, keep_maps=False):
     return res
 
 
+def _frame_roundtrip(frame, params, telemetry, dev):
+    """One numpy frame through the native pipeline: (output array, airlight array).  The
+    frame is staged in pinned memory (H2D asynchronous), the output lands in its own
+    pinned host tensor and is returned as a numpy view of it (budgeted like
+    process_stream's outputs; a plain copy past the budget)."""
+    import torch
+
+    from .engine import FrameEngine
+
+    h, w = int(frame.shape[0]), int(frame.shape[1])
+    OH, OW = FrameEngine.working_size(params, h, w)
+    with torch.cuda.device(dev):
+        hin = torch.empty((1, h, w, 3), dtype=torch.uint8, pin_memory=True)
+        _par_copy(hin[0], torch.from_numpy(frame))
+        din = hin.to(dev, non_blocking=True)
+        out, air = _run_native(din, params, telemetry)[:2]
+        nbytes = OH * OW * 3
+        if nbytes >= _PINNED_OUT_MIN and _pinned_out_take(nbytes):
+            import weakref
+
+            hout = torch.empty((OH, OW, 3), dtype=torch.uint8, pin_memory=True)
+            hair = torch.empty(3, dtype=torch.float64, pin_memory=True)
+            hout.copy_(out[0], non_blocking=True)
+            hair.copy_(air[0], non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+            arr = hout.numpy()
+            weakref.finalize(arr, _pinned_out_release, nbytes)
+            return arr, hair.numpy().copy()
+        return out[0].cpu().numpy(), air[0].cpu().numpy()
+
+
 def _device():
     import torch
 
@@ -300,6 +331,12 @@ def dehaze_frame(frame, params=None, telemetry=None):
 
         out, airlight, maps = dehaze_float_frame(frame if is_tensor else _as_device_batch(frame, dev),
                                                  params, tel)
+    elif not is_tensor and not tel.capture_maps:
+        # numpy in, numpy out: pinned staging in, the output in its own pinned tensor (see
+        # _StreamPipe), one synchronisation; stage events only when the caller asked for them
+        out_np, a_host = _frame_roundtrip(frame, params, telemetry, dev)
+        tel.record_airlight(a_host)
+        return out_np
     else:
         batch = frame[None] if is_tensor else _as_device_batch(frame[None], dev)
         want_maps = tel.capture_maps
@@ -529,7 +566,7 @@ def _par_copy(dst, src):
     list(_pool().map(lambda i: d[cuts[i]:cuts[i + 1]].copy_(s_[cuts[i]:cuts[i + 1]]), range(k)))
 _STREAM_BATCH_MAX = 256
 _PIPE_BATCH_BYTES = 48 << 20      # native path: input bytes per pipelined batch
-_PIPE_SLOTS = 3
+_PIPE_SLOTS = 4                  # one slot's copies pending, three batches in flight (tools/ps_sweep.py)
 # Fresh output frames are handed out as numpy views of their own pinned host tensors (the
 # D2H copy lands in them directly: no staging copy, no first-touch page faults) while the
 # bytes still held by the caller stay under this budget; past it (a sink that keeps every
@@ -613,7 +650,8 @@ class _StreamPipe:
         sdev = [devs[k % len(devs)] for k in range(S)]
         pin = dict(dtype=torch.uint8, pin_memory=True)
         self.hin = [torch.empty((B, H, W, 3), **pin) for _ in range(S)]
-        self.hout = [torch.empty((B, OH, OW, 3), **pin) for _ in range(S)]
+        self.hout = [None] * S   # output staging, allocated on first use (outputs normally own their memory)
+        self._hout_shape = (B, OH, OW, 3)
         self.hair = [torch.empty((B, 3), dtype=torch.float64, pin_memory=True) for _ in range(S)]
         self.din = [torch.empty((B, H, W, 3), dtype=torch.uint8, device=d) for d in sdev]
         self.dout = [torch.empty((B, OH, OW, 3), dtype=torch.uint8, device=d) for d in sdev]
@@ -737,6 +775,8 @@ class _StreamPipe:
                 for i in range(m):
                     own[i].copy_(self.dout[s][i], non_blocking=True)
             else:
+                if self.hout[s] is None:
+                    self.hout[s] = torch.empty(self._hout_shape, dtype=torch.uint8, pin_memory=True)
                 self.hout[s][:m].copy_(self.dout[s][:m], non_blocking=True)
             self.hair[s][:m].copy_(self.dair[s][:m], non_blocking=True)
             self.events[s].record(st)

@@ -270,6 +270,38 @@ class TestPipeline:
         gc.collect()
         assert pl._pinned_out_bytes == base
 
+    def test_frame_outputs_own_their_memory(self, dz, monkeypatch):
+        """dehaze_frame on numpy frames of >= 1 MiB: each result is a view of its own pinned
+        tensor (kept results stay intact across later calls, dropped ones return the budget)
+        and equals the plain-copy form used past the budget and the CUDA-tensor form."""
+        import gc
+
+        import torch
+
+        from paper_2512_16609_b200 import pipeline as pl
+        from paper_2512_16609_b200.synthetic import make_frames
+
+        frames = list(make_frames("c3", frames=4, width=800, height=448).numpy())
+        p = dz.DehazeParams(resize_to=None)
+        gc.collect()
+        base = pl._pinned_out_bytes
+        kept = [dz.dehaze_frame(f, p) for f in frames]
+        assert pl._pinned_out_bytes == base + 4 * frames[0].nbytes
+        assert all(o.dtype == np.uint8 and o.shape == frames[0].shape and o.flags.c_contiguous and o.flags.writeable
+                   for o in kept)
+        snap = [o.copy() for o in kept]
+        monkeypatch.setattr(pl, "_PINNED_OUT_BUDGET", 0)
+        plain = [dz.dehaze_frame(f, p) for f in frames]
+        dev = [dz.dehaze_frame(torch.from_numpy(f).cuda(), p).cpu().numpy() for f in frames]
+        assert all(np.array_equal(a, b) and np.array_equal(a, c) and np.array_equal(a, d)
+                   for a, b, c, d in zip(kept, snap, plain, dev))
+        tel = dz.FrameTelemetry()
+        with_tel = dz.dehaze_frame(frames[0], p, tel)
+        assert np.array_equal(with_tel, kept[0]) and len(tel.airlights) == 1
+        del kept, with_tel
+        gc.collect()
+        assert pl._pinned_out_bytes == base
+
     def test_batch_and_host_batch_match_frame_api(self, dz):
         import torch
 
