@@ -253,15 +253,31 @@ __device__ __forceinline__ double pow_tab(double x, double e, const PowTables& T
 // none: its byte windows are wider than 1/1024) goes to the caller's exact fp64 path.
 constexpr int kByteBuckets = 1024;
 constexpr double kByteMargin = 1e-6;
-// One 16-byte entry per bucket (a single shared-memory load per sample): the lower window
-// (lo(k0), hi(k0)), the upper window's end hi(k0 + 1) and k0 itself; the upper window's
-// start is formed at lookup time as hi(k0) + kByteGap, which is never below lo(k0 + 1):
-// hi(k0) >= thr - margin - ulp and the float sum rounds by at most another ulp (ulp <=
-// 6e-8 below 1), so hi(k0) + 2.2e-6 >= thr + margin + 8e-8.
+// One 8-byte entry per bucket (a single 64-bit shared-memory load per sample):
+//   x = hi(k0), the end of the lower window.  Its start lo(k0) is not stored: a sample in
+//       bucket j is >= j/1024, so lo(k0) <= j/1024 makes the test redundant; the rare
+//       bucket whose lower threshold lies within the margin below its start gets x = NaN
+//       (both windows reject, every sample of it takes the exact path);
+//   y = hi(k0 + 1), the end of the upper window, moved down by < 512 ulps so that its low
+//       8 bits hold k0 (smaller is conservative).
+// The upper window's start is formed at lookup time as hi(k0) + kByteGap, which is never
+// below lo(k0 + 1): hi(k0) >= thr - margin - ulp and the float sum rounds by at most
+// another ulp (ulp <= 6e-8 below 1), so hi(k0) + 2.2e-6 >= thr + margin + 8e-8.
 constexpr float kByteGap = 2.2e-6f;
 struct ByteBuckets {
-  float4 ent[kByteBuckets + 1];  // (lo(k0), hi(k0), hi(k0 + 1), bits: k0)
+  float2 ent[kByteBuckets + 1];
 };
+
+// f moved down (towards -inf) until its low 8 bits equal k (k < 256)
+__device__ __forceinline__ float byte_tag_down(float f, uint32_t k) {
+  const uint32_t bits = __float_as_uint(f);
+  if (bits & 0x80000000u) {  // negative: a larger magnitude is further down
+    const uint32_t mag = bits & 0x7FFFFFFFu;
+    return __uint_as_float(0x80000000u | (((mag + 256u) & ~255u) | k));
+  }
+  if (bits < 256u) return __uint_as_float(0x80000000u | 256u | k);  // below the smallest taggable positive
+  return __uint_as_float(((bits - 256u) & ~255u) | k);
+}
 
 // Block-cooperative build from thr[0..255] (thr[0] unused; +inf = unreachable level);
 // the caller synchronises before use.
@@ -278,16 +294,18 @@ __device__ __forceinline__ void byte_buckets_build(ByteBuckets& B, const double*
       if (thr[mid] <= x) lo = mid;
       else hi = mid - 1;
     }
-    B.ent[j] = make_float4(lo_of(lo), hi_of(lo), hi_of(lo + 1), __uint_as_float((uint32_t)lo));
+    const bool lower_ok = (double)lo_of(lo) <= x;  // (-inf for lo == 0)
+    B.ent[j] = make_float2(lower_ok ? hi_of(lo) : __uint_as_float(0x7FC00000u),
+                           byte_tag_down(hi_of(lo + 1), (uint32_t)lo));
   }
 }
 
 // Byte of xf from the table; ok stays true only if xf lies inside an acceptance window.
 __device__ __forceinline__ uint32_t byte_bucket(const ByteBuckets& B, float xf, bool& ok) {
   const uint32_t j = min(__float2uint_rd(xf * (float)kByteBuckets), (uint32_t)kByteBuckets);  // (negative -> 0)
-  const float4 e = B.ent[j];
-  const uint32_t k = __float_as_uint(e.w);
-  const bool in0 = xf >= e.x && xf < e.y, in1 = xf >= e.y + kByteGap && xf < e.z;
+  const float2 e = B.ent[j];
+  const uint32_t k = __float_as_uint(e.y) & 255u;
+  const bool in0 = xf < e.x, in1 = xf >= e.x + kByteGap && xf < e.y;
   ok = ok && (in0 || in1);
   return k + (in1 ? 1u : 0u);
 }
