@@ -208,6 +208,30 @@ def test_k1_tma_variant(oracle, r, monkeypatch):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("shape", [(5, 130, 976), (2, 720, 1280), (1, 16, 16)])
+def test_k6_ring_variant(oracle, shape, monkeypatch):
+    """DHZ_K6_RING=1: K6 with the frame bytes staged by cp.async.bulk into a two-stage
+    shared-memory ring (mbarrier full/empty pairs): several frames per CTA, blocks that
+    end inside a stage, a single 16-unit frame; bytes identical to the LDG form and to
+    the direct-gather form, and checked against the oracle."""
+    n, H, W = shape
+    rng = np.random.default_rng(4100 + n)
+    frames = rng.integers(0, 256, size=(n, H, W, 3), dtype=np.uint8)
+    frames[0, : H // 2] = np.clip(frames[0, : H // 2].astype(np.int16) // 4 + 150, 0, 255).astype(np.uint8)
+    p = _params()
+    monkeypatch.setenv("DHZ_K6_DIRECT", "0")
+    base = _run(frames, p)
+    monkeypatch.setenv("DHZ_K6_RING", "1")
+    ring = _run(frames, p)
+    monkeypatch.setenv("DHZ_K6_DIRECT", "1")
+    direct = _run(frames, p)
+    for a, b, c in zip(base, ring, direct):
+        assert np.array_equal(a, b) and np.array_equal(a, c)
+    monkeypatch.setenv("DHZ_K6_DIRECT", "0")
+    if n * H * W <= 2_000_000:
+        _check(frames, p, oracle)
+
+
 def test_balance_out_of_band_samples(oracle):
     # uniform noise: most non-minimum samples lie >= 64 levels above their pixel's
     # minimum, outside the banded table (k_balance_band's per-unit correction path)
