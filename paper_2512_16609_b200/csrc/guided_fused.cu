@@ -1075,14 +1075,18 @@ __device__ __forceinline__ void x_ab_segment(const FusedArgs& A, const FusedShar
     uint64_t* const tw = e2 + 2 * kXCols;
     x_scan3<Q3T>(L.q1, L.q2, L.q3, e1, e2, e3, tw, tw + kXTw, reinterpret_cast<Q3T*>(tw + 2 * kXTw));
     if (G.need && y + 1 < y1) {  // slide the window one row down while the others scan
-      const uint32_t wE[3] = {nE[0], nE[1], nE[2]}, wL[3] = {nL[0], nL[1], nL[2]};
+      // The next step's rows are loaded into nE / nL right after this step's features have
+      // consumed them (same registers, dead by then): the loads then have the rest of the
+      // step and the next scan to land.  (Loading before the features made the compiler
+      // rotate two register sets with moves at the end of this block, which waited for
+      // the loads there: 7 % of the kernel's stall samples on one IMAD.MOV.)
+      Feat<CLIP> fe, fl;
+      features<CLIP>(nE, S.mstar, fe);
+      features<CLIP>(nL, S.mstar, fl);
       if (y + 2 < y1) {
         load_row(nE, frame, pitch, CL(y + r + 2), G.xt, W, vec);
         load_row(nL, frame, pitch, CL(y - r + 1), G.xt, W, vec);
       }
-      Feat<CLIP> fe, fl;
-      features<CLIP>(wE, S.mstar, fe);
-      features<CLIP>(wL, S.mstar, fl);
       accumulate<CLIP>(L, &fe, &fl);
     }
     __syncthreads();
