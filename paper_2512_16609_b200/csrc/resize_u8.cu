@@ -562,14 +562,18 @@ __global__ void __launch_bounds__(kT3)
 k_rs_recover(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const double* __restrict__ airlight,
              double omega, double t_min, const double* __restrict__ thr, const float* __restrict__ gains,
              double inv_gamma, int gamma_is_one, uint8_t* __restrict__ out, int64_t out_fs,
-             double* __restrict__ part) {
+             double* __restrict__ part, int nframes) {
   __shared__ double s_f[256];
   __shared__ double s_thr[MODE == 2 ? 3 : 1][256];
   __shared__ double red[3][kT3 / 32];
   __shared__ TapS s_tx[kColTab];
   __shared__ PowTables PT;  // balance sums (MODE 1)
   __shared__ ByteBuckets BK;  // fp32 fast path of the bytes (MODE 0)
-  const int f = blockIdx.y;
+  // MODE 0 (nframes > 0): persistent CTAs over the batch's flat (frame, row) space — the
+  // tables do not depend on the frame, so a CTA walks from frame to frame and every SM
+  // keeps the same number of resident CTAs to the end (a (row block, frame) grid left a
+  // thin last wave).  MODE 1 / 2: blockIdx.y is the frame, blockIdx.x its row block.
+  int f = (MODE == 0) ? 0 : (int)blockIdx.y;
   s_f[threadIdx.x] = u8f(threadIdx.x);
   if (MODE == 1) pow_tables_init(PT);
   if (MODE == 0) s_thr[0][threadIdx.x] = thr[threadIdx.x];
@@ -580,11 +584,23 @@ k_rs_recover(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const d
     byte_buckets_build(BK, s_thr[0]);
     __syncthreads();
   }
+  const float ig = (float)inv_gamma;
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  // flat rows [q0, q1) (MODE 0: of the batch; else of the frame); column taps tabulated once per CTA
+  const int64_t rows = (MODE == 0) ? (int64_t)nframes * G.H : (int64_t)G.H;
+  const int64_t q0 = rows * blockIdx.x / gridDim.x, q1 = rows * (blockIdx.x + 1) / gridDim.x;
+  const bool tab = G.W <= kColTab;
+  for (int x = threadIdx.x; tab && x < G.W; x += kT3) s_tx[x] = compact(tap(x, G.sx, G.w));
+  __syncthreads();
+  for (int64_t q = q0; q < q1;) {
+  if (MODE == 0) f = (int)(q / G.H);
+  const int r0 = (int)(q - (int64_t)(MODE == 0 ? f : 0) * G.H);
+  const int r1 = (int)min((int64_t)G.H, r0 + (q1 - q));
+  q += r1 - r0;
   const double A0 = airlight[3 * f], A1 = airlight[3 * f + 1], A2 = airlight[3 * f + 2];
   const double amax = dmax(dmax(A0, A1), A2);
   const double ramax = __drcp_rn(amax);  // cmin / amax as the exact div_rb
   const float af0 = (float)A0, af1 = (float)A1, af2 = (float)A2;
-  const float ig = (float)inv_gamma;
   float g0 = 1.0f, g1 = 1.0f, g2 = 1.0f;
   if (MODE == 2) {
     g0 = gains[3 * f];
@@ -593,12 +609,6 @@ k_rs_recover(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const d
   }
   const uint8_t* frame = in + (int64_t)f * in_fs;
   uint8_t* fo = out + (int64_t)f * out_fs;
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-  // rows [r0, r1) of the output; column taps tabulated once per CTA
-  const int r0 = (int)((int64_t)G.H * blockIdx.x / gridDim.x), r1 = (int)((int64_t)G.H * (blockIdx.x + 1) / gridDim.x);
-  const bool tab = G.W <= kColTab;
-  for (int x = threadIdx.x; tab && x < G.W; x += kT3) s_tx[x] = compact(tap(x, G.sx, G.w));
-  __syncthreads();
   for (int y = r0; y < r1; ++y)
   for (int x = threadIdx.x; x < G.W; x += kT3) {
     const int64_t p = (int64_t)y * G.W + x;
@@ -651,6 +661,7 @@ k_rs_recover(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const d
       o[2] = (uint8_t)quantize_thr_from(x2, t2, guess_byte(x2, ig, g2));
     }
   }
+  }  // flat row ranges
   if (MODE == 1) {
     double v3[3] = {acc0, acc1, acc2};
 #pragma unroll
@@ -730,21 +741,24 @@ cudaError_t resize_recover(const uint8_t* in, int64_t in_fs, int n, const Resize
   const double ig = 1.0 / gamma;
   const int g1 = gamma == 1.0 ? 1 : 0;
   if (!balance) {
-    const int64_t want = std::max<int64_t>(1, (8LL * sm_count() + n - 1) / std::max(n, 1));
-    const int bx = (int)std::max<int64_t>(1, std::min<int64_t>(g.H, want));  // row blocks per frame
-    k_rs_recover<0><<<dim3(bx, n), kT3, 0, st>>>(in, in_fs, g, airlight, omega, t_min, thr, nullptr, ig, g1, out,
-                                                 out_fs, nullptr);
+    // persistent: every SM's full complement of CTAs over the batch's flat rows (at least ~2 rows each)
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rs_recover<0>, kT3, 0);
+    const int64_t rows = (int64_t)n * g.H;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(occ, 1) * sm_count(), (rows + 1) / 2));
+    k_rs_recover<0><<<grid, kT3, 0, st>>>(in, in_fs, g, airlight, omega, t_min, thr, nullptr, ig, g1, out, out_fs,
+                                          nullptr, n);
     return cudaGetLastError();
   }
   double* part = static_cast<double*>(bal_ws);
   double* bthr = part + (size_t)n * kResizeSumParts * 3;
   float* gains = reinterpret_cast<float*>(bthr + (size_t)n * 3 * 256);
   k_rs_recover<1><<<dim3(kResizeSumParts, n), kT3, 0, st>>>(in, in_fs, g, airlight, omega, t_min, nullptr, nullptr,
-                                                            ig, g1, out, out_fs, part);
+                                                            ig, g1, out, out_fs, part, n);
   cudaError_t e = balance_thresholds(part, kResizeSumParts, n, npx, gamma, bthr, gains, st);
   if (e != cudaSuccess) return e;
   k_rs_recover<2><<<dim3(kResizeSumParts, n), kT3, 0, st>>>(in, in_fs, g, airlight, omega, t_min, bthr, gains, ig,
-                                                            g1, out, out_fs, nullptr);
+                                                            g1, out, out_fs, nullptr, n);
   return cudaGetLastError();
 }
 
