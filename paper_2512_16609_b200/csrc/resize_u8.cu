@@ -35,7 +35,7 @@ namespace {
 
 constexpr int kTH = 32, kTW = 64;   // R1 output tile
 constexpr int kT1 = 256;            // R1 threads
-constexpr int kT2 = 1024;           // R2 threads
+constexpr int kT2 = 512;            // R2 threads (4 CTAs/SM: a 300-frame batch is one wave; 1024 ran it as 148 + 148 + 4)
 constexpr int kCap = 4096;          // R2 candidates kept in shared memory
 constexpr int kT3 = 256;            // R3 threads
 constexpr int kColTab = 1024;       // R3: output widths up to this use a column-tap table
@@ -424,7 +424,7 @@ __device__ void select_ordered(const Get& get, const Idx& idx, int64_t m, double
   }
 }
 
-__global__ void __launch_bounds__(kT2)
+__global__ void __launch_bounds__(kT2, 3)
 k_rs_select(const uint8_t* __restrict__ in, int64_t in_fs, ResizeGeo G, const double* __restrict__ dark,
             const uint32_t* __restrict__ hist, int64_t K, double alpha, uint32_t* __restrict__ sel_all,
             double* __restrict__ airlight) {
