@@ -94,6 +94,18 @@ def _ncu_traffic_per_px():
         return {}
 
 
+def _ncu_guided_traffic_per_px(balance):
+    """DRAM bytes per pixel of the image-mode guided stage (its kernels summed) from the committed
+    ncu launch list of the C5 bench command (profiles/ncu_traffic_c5.json); None if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_c5.json")) as fh:
+            ks = json.load(fh)["kernels"]
+        names = ["k_gx_ab", "k_gx_out"] + (["k_gw_sums", "k_gf_thresholds", "k_gf_apply2"] if balance else [])
+        return sum(float(ks[k]["dram_bytes_per_px"]) for k in names if k in ks)
+    except Exception:
+        return None
+
+
 def _calibration(cfg):
     """Real reference vs the oracle port on identical frames (tools/calibrate_cpu_baseline.py, run
     where /root/reference exists; one thread each): how much slower the reference itself is."""
@@ -482,6 +494,10 @@ def main():
                 "achieved": round(g_gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(g_gbs / peak, 4),
                 "traffic": None, "peak_kind": peak_kind, "alg_bytes_per_launch": gb,
                 "launch_ms": round(stage_ms[2], 4)}
+        tpx = _ncu_guided_traffic_per_px(params.balance_enabled()) if _base(cfg) == "c5" else None
+        if tpx is not None:  # measured on C5 frames (8K, r = 60); other geometries differ, so C2 stays null
+            roof["traffic"] = int(round(tpx * n * npx))
+            roof["traffic_source"] = "profiles/ncu_traffic_c5.json (ncu dram__bytes_read+write per px, stage kernels summed)"
         # K1 + the 6 select kernels + pass1 + pass2 (+ sums, thresholds, apply) per <=12 GB chunk of frames
         launches = 7 + (5 if params.balance_enabled() else 2) * math.ceil(n / _guided_chunk(n, H, W, params))
     else:
